@@ -1,0 +1,144 @@
+/*
+ * h2g.h — C ABI of the B200-native H2* / (H2+H)* matrix-vector product.
+ *
+ * This is the drop-in boundary for the reference's operator object.  The
+ * reference (pkg/src/h2weak, pure Python) has no FFI; its operator interface
+ * is duck-typed Python:
+ *
+ *   HierRep.matvec(q) -> phi            engine.py:250-269   -> h2g_matvec / h2g_matvec_host
+ *   compute_potential(rep, q)           engine.py:321-322   -> h2g_matvec_host
+ *   BlockLowRankRep.matvec(q)           blr.py:32-33        -> (BLR leg inside the plan)
+ *   build_variant(...) -> HierRep       engine.py:325-373   -> h2g_plan_create (from the
+ *                                                              packed export of that rep)
+ *   rep.mem_scalars                     engine.py:184-186   -> h2g_plan_stats.mem_scalars
+ *
+ * The Python host (paper_2309_14085_b200/gpu_rep.py) binds these with ctypes
+ * and exposes GpuHierRep.matvec with the reference's contract (same
+ * ValueError("vector length mismatch"), fp64 promotion, fresh output).
+ *
+ * Conventions
+ *  - All arrays in h2g_export_desc are HOST pointers owned by the caller;
+ *    h2g_plan_create copies what it needs to the device, so they may be freed
+ *    after it returns.  The plan owns all device memory it allocates.
+ *  - Vectors are in ORIGINAL point order (the plan applies the tree
+ *    permutation itself).  nrhs right-hand sides are stored point-major:
+ *    element (i, j) at q[i * ld + j] (a C-contiguous N x nrhs array).
+ *  - Return codes: 0 = OK, otherwise an H2G_ERR_* code; h2g_error_string()
+ *    gives a static message and h2g_last_error_detail() a per-thread detail.
+ *  - Threading: one plan = one CUDA stream of work; matvec calls on the same
+ *    plan must not run concurrently (the coefficient workspace is shared).
+ */
+#ifndef H2G_H
+#define H2G_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define H2G_ABI_VERSION 1
+
+enum {
+  H2G_OK = 0,
+  H2G_ERR_LENGTH_MISMATCH = 1, /* -> ValueError("vector length mismatch") (engine.py:253-254) */
+  H2G_ERR_BAD_EXPORT = 2,      /* inconsistent packed export */
+  H2G_ERR_CUDA = 3,            /* CUDA runtime error (detail has the CUDA message) */
+  H2G_ERR_NO_DEVICE = 4,       /* no usable sm_100 device */
+  H2G_ERR_INVALID_ARG = 5,
+  H2G_ERR_OOM = 6
+};
+
+/* One nested channel (reference NestedOperatorSet, engine.py:117-130).
+ * Offsets index the fp64 blob (in doubles); -1 = operator absent.
+ * All matrices column-major. */
+typedef struct h2g_channel_desc {
+  const int32_t* r_in;        /* [n_clusters] incoming rank (PivotQuad.rank_in, lowrank.py:53-55) */
+  const int32_t* r_out;       /* [n_clusters] outgoing rank (lowrank.py:57-59) */
+  const int64_t* p2m_off;     /* [n_clusters] r_out x n_X            ops.p2m[X]        */
+  const int64_t* l2p_off;     /* [n_clusters] n_X x r_in             ops.l2p[X]        */
+  const int64_t* m2m_off;     /* [n_clusters] r_out(P) x r_out(c)    ops.m2m[(P, c)]   keyed by child c */
+  const int64_t* l2l_off;     /* [n_clusters] r_in(c) x r_in(P)      ops.l2l[(c, P)]   keyed by child c */
+  const int64_t* m2l_rowptr;  /* [n_clusters + 1] CSR by target X                      */
+  const int32_t* m2l_src;     /* [nnz] source Y, lists_fn order (partition.py:133-136) */
+  const int64_t* m2l_off;     /* [nnz] r_in(X) x r_out(Y)            ops.m2l[(X, Y)]   */
+} h2g_channel_desc;
+
+/* The packed export (paper_2309_14085_b200/packed.py, SURVEY.md §8(a')). */
+typedef struct h2g_export_desc {
+  int32_t abi_version;        /* H2G_ABI_VERSION */
+  int32_t dim;                /* 1..3 */
+  int32_t kappa;              /* tree depth (tree.py:140-143) */
+  int32_t n_channels;         /* 0..2 nested channels (h2star-bt: 2, h2plusH-star: 1) */
+  int64_t n_points;           /* N */
+  int64_t n_clusters;         /* level_offset[kappa + 1] */
+  int64_t mem_scalars;        /* reference tally (engine.py:184-186, 315; blr.py:59) */
+  const int64_t* perm;        /* [N] tree position -> original index (tree.py:152-165) */
+  const int64_t* level_offset;/* [kappa + 2] (tree.py:72-75) */
+  const int64_t* cl_start;    /* [n_clusters] tree-order slice of every cluster */
+  const int64_t* cl_end;
+  h2g_channel_desc channels[2];
+  /* BLR leg of (H2+H)* (blr.py:72-83): CSR by target over rank>0 factors */
+  const int64_t* blr_rowptr;  /* [n_clusters + 1] */
+  const int32_t* blr_src;     /* [nnz] */
+  const int32_t* blr_rank;    /* [nnz] p */
+  const int64_t* blr_u_off;   /* [nnz] U: n_X x p column-major */
+  const int64_t* blr_v_off;   /* [nnz] V: n_Y x p row-major (= V^T column-major) */
+  /* near field (engine.py:260-268): CSR by target leaf */
+  const int64_t* near_rowptr; /* [n_clusters + 1] */
+  const int32_t* near_src;    /* [nnz] */
+  const int64_t* near_off;    /* [nnz] n_X x n_Y column-major */
+  int64_t blob_len;           /* doubles */
+  const double* blob;         /* all operator matrices */
+} h2g_export_desc;
+
+typedef struct h2g_plan h2g_plan;
+
+typedef struct h2g_plan_stats {
+  int64_t n_points;
+  int64_t mem_scalars;         /* reference tally */
+  int64_t alg_bytes;           /* 8 * mem_scalars + 16 * N */
+  int64_t blob_bytes;          /* device bytes of the operator blob (incl. alignment) */
+  int64_t workspace_bytes;     /* coefficient arena + task tables */
+  int32_t n_phases;            /* device phases per matvec */
+  int32_t n_launches;          /* kernel launches per single-RHS matvec */
+  int64_t n_tasks;
+  int64_t n_terms;
+  int32_t device;
+  int32_t graph;               /* 1 if the fixed phases run as one CUDA graph */
+} h2g_plan_stats;
+
+/* Build a plan (upload + schedule) for one operator on CUDA device `device`. */
+int h2g_plan_create(const h2g_export_desc* desc, int device, h2g_plan** out);
+int h2g_plan_destroy(h2g_plan* plan);
+int h2g_plan_get_stats(const h2g_plan* plan, h2g_plan_stats* out);
+
+/* phi = K q for nrhs right-hand sides, DEVICE pointers, stream-ordered on
+ * `stream` (a cudaStream_t used as given: NULL = the legacy default stream,
+ * as everywhere in CUDA); no host sync. */
+int h2g_matvec(h2g_plan* plan, const double* q_dev, double* phi_dev, int64_t n,
+               int64_t nrhs, int64_t ld, void* stream);
+
+/* Same with HOST pointers: H2D copy, matvec, D2H copy, synchronous
+ * (the reference's call shape, engine.py:250-269). */
+int h2g_matvec_host(h2g_plan* plan, const double* q_host, double* phi_host, int64_t n,
+                    int64_t nrhs, int64_t ld);
+
+/* Per-phase device timing: runs `iters` matvecs phase by phase with CUDA events
+ * on the plan's stream.  ms[i] = mean duration of phase i, bytes[i] = its
+ * algorithmic bytes, names[i] = static name.  Up to `cap` phases are written;
+ * returns the number of phases through *n_out. */
+int h2g_profile_phases(h2g_plan* plan, const double* q_dev, double* phi_dev, int iters,
+                       double* ms, int64_t* bytes, const char** names, int cap, int* n_out);
+
+/* Number of kernels a single-RHS matvec launches (for bench gpu_launches). */
+int h2g_launches_per_matvec(const h2g_plan* plan, int64_t nrhs);
+
+const char* h2g_error_string(int code);
+const char* h2g_last_error_detail(void);
+int h2g_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2G_H */

@@ -1,0 +1,55 @@
+"""In-tree build of the native libraries (sm_100a).
+
+    python -m paper_2309_14085_b200.build
+
+produces ``paper_2309_14085_b200/lib/libh2g.so`` (CUDA matvec, include/h2g.h).
+The .so files are git-ignored but travel to the GPU box with the snapshot.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIBDIR = os.path.join(PKG, "lib")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+           "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+
+TARGETS = {
+    "libh2g.so": (["h2g_plan.cu"], ["h2g_kernels.cuh"]),
+}
+
+
+def _stale(out, srcs):
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(s) > t for s in srcs)
+
+
+def build(force: bool = False, verbose: bool = True) -> dict:
+    os.makedirs(LIBDIR, exist_ok=True)
+    built = {}
+    for name, (srcs, deps) in TARGETS.items():
+        out = os.path.join(LIBDIR, name)
+        src_paths = [os.path.join(CSRC, s) for s in srcs]
+        dep_paths = src_paths + [os.path.join(CSRC, s) for s in deps] + [
+            os.path.join(ROOT, "include", "h2g.h")]
+        if force or _stale(out, dep_paths):
+            cmd = [NVCC, *ARCH, *NVFLAGS, "-shared", "-o", out, *src_paths]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            subprocess.run(cmd, check=True)
+        built[name] = out
+    return built
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

@@ -1,0 +1,153 @@
+// h2g_kernels.cuh — device code of the H2* / (H2+H)* matvec (sm_100a).
+//
+// Every phase of the reference MVP (engine.py:190-269) is a batch of
+// gather-by-target GEMV *tasks*: task t owns a disjoint output slice
+// y[0:m) of the coefficient arena and computes
+//
+//     y = sum_{terms k of t}  A_k (m x ncols_k, column-major, leading dim lda_k)
+//                               * x_k (ncols_k contiguous arena slots)
+//
+// P2M, M2M, M2L(+L2L), L2P, the BLR leg and the near field are all instances
+// (see h2g_plan.cu for the mapping).  One CTA runs one task; its warps split
+// each term's columns in groups of kUnroll, every lane owns rows lane+32j, so
+// each column is read with one coalesced request per 32 rows and no
+// cross-lane reduction is needed.  Warps are combined through shared memory
+// in a fixed order and the result is stored once: no atomics, deterministic
+// summation order (SURVEY.md §7 hard part 2).
+#pragma once
+#include <cstdint>
+
+namespace h2g {
+
+struct Task {          // 24 bytes
+  int64_t y_off;       // arena slot of y[0]
+  int32_t m;           // rows (<= kMaxRows)
+  int32_t t_begin;     // term range [t_begin, t_end) -- int32 is enough per phase
+  int32_t t_end;
+  int32_t pad;
+};
+
+struct Term {          // 24 bytes
+  int64_t a_off;       // blob offset (doubles) of A(0, 0)
+  int64_t x_off;       // arena slot of x[0]
+  int32_t lda;         // column stride of A in doubles
+  int32_t ncols;
+};
+
+struct ReduceJob {     // BLR split-K partials -> w, fixed order
+  int64_t w_off;
+  int64_t part_off;    // partials: chunk c at part_off + c * p
+  int32_t p;
+  int32_t chunks;
+};
+
+constexpr int kMaxJ = 8;         // rows per lane -> m <= 256 per task
+constexpr int kMaxRows = 32 * kMaxJ;
+constexpr int kWarps = 4;        // warps per CTA (one task per CTA)
+constexpr int kUnroll = 4;       // columns in flight per warp iteration
+
+__device__ __forceinline__ double ld_stream(const double* p) {
+  // operator entries are touched exactly once per matvec: evict-first
+  return __ldcs(p);
+}
+
+template <int J>
+__device__ __forceinline__ void term_accumulate(const double* __restrict__ A, int lda,
+                                                int ncols, const double* __restrict__ x,
+                                                int m, int lane, int warp, double (&acc)[J]) {
+  // warp w takes column groups [g*kUnroll, g*kUnroll + kUnroll) with g = w, w+kWarps, ...
+  for (int c0 = warp * kUnroll; c0 < ncols; c0 += kWarps * kUnroll) {
+    double a[kUnroll][J];
+    double xv[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const int c = c0 + k;
+      const bool cv = c < ncols;
+      xv[k] = cv ? __ldg(x + c) : 0.0;
+      const double* col = A + (int64_t)c * lda;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int r = lane + 32 * j;
+        a[k][j] = (cv && r < m) ? ld_stream(col + r) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k)
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[j] = fma(a[k][j], xv[k], acc[j]);
+  }
+}
+
+template <int J>
+__device__ __forceinline__ void run_task(const Task& tk, const Term* __restrict__ terms,
+                                         const double* __restrict__ blob, double* arena,
+                                         double* red /* smem [kWarps][32*J] */) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double acc[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) acc[j] = 0.0;
+  for (int t = tk.t_begin; t < tk.t_end; ++t) {
+    const Term tm = terms[t];
+    term_accumulate<J>(blob + tm.a_off, tm.lda, tm.ncols, arena + tm.x_off, tk.m, lane, warp,
+                       acc);
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) red[warp * (32 * J) + lane + 32 * j] = acc[j];
+  __syncthreads();
+  double* y = arena + tk.y_off;
+  for (int r = threadIdx.x; r < tk.m; r += blockDim.x) {
+    double s = red[r];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) s += red[w * (32 * J) + r];
+    y[r] = s;
+  }
+}
+
+// One CTA per task.  Rows-per-lane J is chosen per task at run time and
+// dispatched to a compile-time instance so accumulators stay in registers.
+__global__ void __launch_bounds__(kWarps * 32)
+gemv_tasks_kernel(const Task* __restrict__ tasks, const Term* __restrict__ terms,
+                  const double* __restrict__ blob, double* arena) {
+  __shared__ double red[kWarps * kMaxRows];
+  const Task tk = tasks[blockIdx.x];
+  const int J = (tk.m + 31) >> 5;
+  if (J <= 1)      run_task<1>(tk, terms, blob, arena, red);
+  else if (J == 2) run_task<2>(tk, terms, blob, arena, red);
+  else if (J <= 4) run_task<4>(tk, terms, blob, arena, red);
+  else             run_task<8>(tk, terms, blob, arena, red);
+}
+
+// q_tree[i] = q[perm[i] * ld]  (tree order gather, reference q[index_set])
+__global__ void gather_perm_kernel(const double* __restrict__ q, int64_t ld,
+                                   const int32_t* __restrict__ perm, double* __restrict__ out,
+                                   int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = q[(int64_t)perm[i] * ld];
+}
+
+// phi[perm[i] * ld] = phi_tree[i]  (reference phi[index_set] +=, disjoint slices)
+__global__ void scatter_perm_kernel(const double* __restrict__ in,
+                                    const int32_t* __restrict__ perm, double* __restrict__ phi,
+                                    int64_t ld, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    phi[(int64_t)perm[i] * ld] = in[i];
+}
+
+// w[i] = sum_c part[c * p + i], c ascending (deterministic split-K reduce)
+__global__ void reduce_partials_kernel(const ReduceJob* __restrict__ jobs, int n_jobs,
+                                       double* arena) {
+  const int j = blockIdx.x;
+  if (j >= n_jobs) return;
+  const ReduceJob jb = jobs[j];
+  for (int i = threadIdx.x; i < jb.p; i += blockDim.x) {
+    const double* part = arena + jb.part_off + i;
+    double s = 0.0;
+    for (int c = 0; c < jb.chunks; ++c) s += part[(int64_t)c * jb.p];
+    arena[jb.w_off + i] = s;
+  }
+}
+
+}  // namespace h2g

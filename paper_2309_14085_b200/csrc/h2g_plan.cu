@@ -1,0 +1,667 @@
+// h2g_plan.cu — plan compiler + C ABI (include/h2g.h) for the B200 matvec.
+//
+// h2g_plan_create turns the packed export (SURVEY.md §8(a')) into a fixed
+// schedule of device phases, each a batch of gather-by-target GEMV tasks
+// (h2g_kernels.cuh).  Mapping onto the reference MVP (engine.py:190-269):
+//
+//   phase            reference                      task = one output slice
+//   ---------------  -----------------------------  --------------------------------------
+//   gather           q[X.index_set]                 q_tree = q[perm]
+//   up_leaf          P2M   engine.py:194-197        v_ch[X] = P2M_X q_tree[X]   (all channels)
+//                    BLR   blr.py:83 (V^H q)        w_XY (or a split-K chunk) = V^T q_tree[Y]
+//   blr_reduce       (split-K partials, fixed order)
+//   m2m_l (l=k-1..1) M2M   engine.py:198-208        v[X] = sum_c M2M_Xc v[c]
+//   down_l (l=1..k)  M2L   engine.py:209-220        u[X] = sum_Y M2L_XY v[Y] + L2L_X u[parent(X)]
+//                    L2L   engine.py:221-228          (L2L fused as the last term)
+//   leaf             L2P   engine.py:229-232        phi_tree[X] = sum_ch L2P_X u_ch[X]
+//                    BLR   blr.py:83 (U w)            + sum_{A ancestor-or-self, Y} U_AY[rows X] w_AY
+//                    near  engine.py:260-268          + sum_Y K_XY q_tree[Y]
+//   scatter          phi[X.index_set] = ...         phi = phi_tree[perm^-1]
+//
+// Each output is written by exactly one task, so the whole matvec is
+// atomic-free and bitwise repeatable.  The middle phases are captured once
+// into a CUDA graph.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/h2g.h"
+#include "h2g_kernels.cuh"
+
+using namespace h2g;
+
+namespace {
+
+thread_local std::string g_detail;
+
+int fail(int code, const std::string& msg) {
+  g_detail = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                               \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return fail(_e == cudaErrorMemoryAllocation ? H2G_ERR_OOM : H2G_ERR_CUDA,      \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));               \
+  } while (0)
+
+enum PhaseKind { PH_GEMV = 0, PH_REDUCE = 1 };
+
+struct Phase {
+  int kind;
+  std::string name;
+  int64_t task_begin = 0, task_end = 0;  // into d_tasks (GEMV) or d_jobs (REDUCE)
+  int64_t alg_bytes = 0;                 // operator + vector bytes (algorithmic)
+};
+
+struct HostSchedule {
+  std::vector<Task> tasks;
+  std::vector<Term> terms;
+  std::vector<ReduceJob> jobs;
+  std::vector<Phase> phases;
+  // terms of the task currently being built (before row splitting)
+  std::vector<Term> cur;
+};
+
+constexpr int kBlrChunkDoubles = 16384;  // split-K chunk of a BLR V^T q product
+
+}  // namespace
+
+struct h2g_plan {
+  int device = 0;
+  int64_t N = 0;
+  int64_t mem_scalars = 0;
+  int64_t n_slots = 0;
+  int64_t q_tree = 0, phi_tree = 0;
+  cudaStream_t stream = nullptr;
+  double* d_blob = nullptr;
+  int64_t blob_len = 0;
+  double* d_arena = nullptr;
+  int32_t* d_perm = nullptr;
+  Task* d_tasks = nullptr;
+  Term* d_terms = nullptr;
+  ReduceJob* d_jobs = nullptr;
+  std::vector<Phase> phases;
+  int64_t n_tasks = 0, n_terms = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  int64_t workspace_bytes = 0;
+};
+
+namespace {
+
+// Emit the task being built (rows y[0:m)), splitting rows into <= kMaxRows
+// pieces; every piece keeps the same terms shifted by its first row.
+void emit_task(HostSchedule& s, int64_t y_off, int64_t m, int64_t& bytes) {
+  for (int64_t r0 = 0; r0 < m; r0 += kMaxRows) {
+    const int32_t mm = (int32_t)std::min<int64_t>(kMaxRows, m - r0);
+    Task t;
+    t.y_off = y_off + r0;
+    t.m = mm;
+    t.t_begin = (int32_t)s.terms.size();
+    for (const Term& tm : s.cur) {
+      Term u = tm;
+      u.a_off += r0;
+      s.terms.push_back(u);
+      bytes += 8LL * mm * tm.ncols;
+    }
+    t.t_end = (int32_t)s.terms.size();
+    t.pad = 0;
+    s.tasks.push_back(t);
+  }
+  for (const Term& tm : s.cur) bytes += 8LL * tm.ncols;  // x reads
+  bytes += 8LL * m;                                       // y write
+  s.cur.clear();
+}
+
+void add_term(HostSchedule& s, int64_t a_off, int64_t x_off, int64_t lda, int64_t ncols) {
+  if (ncols <= 0) return;
+  Term t;
+  t.a_off = a_off;
+  t.x_off = x_off;
+  t.lda = (int32_t)lda;
+  t.ncols = (int32_t)ncols;
+  s.cur.push_back(t);
+}
+
+void begin_phase(HostSchedule& s, int kind, const std::string& name) {
+  Phase p;
+  p.kind = kind;
+  p.name = name;
+  p.task_begin = kind == PH_GEMV ? (int64_t)s.tasks.size() : (int64_t)s.jobs.size();
+  s.phases.push_back(p);
+}
+
+void end_phase(HostSchedule& s) {
+  Phase& p = s.phases.back();
+  p.task_end = p.kind == PH_GEMV ? (int64_t)s.tasks.size() : (int64_t)s.jobs.size();
+  if (p.task_end == p.task_begin) s.phases.pop_back();  // nothing to run
+}
+
+int validate(const h2g_export_desc* d) {
+  if (!d) return fail(H2G_ERR_INVALID_ARG, "null export descriptor");
+  if (d->abi_version != H2G_ABI_VERSION)
+    return fail(H2G_ERR_BAD_EXPORT, "abi_version mismatch");
+  if (d->dim < 1 || d->dim > 3 || d->kappa < 1 || d->n_channels < 0 || d->n_channels > 2)
+    return fail(H2G_ERR_BAD_EXPORT, "dim/kappa/n_channels out of range");
+  if (d->n_points <= 0 || d->n_points >= (1LL << 31))
+    return fail(H2G_ERR_BAD_EXPORT, "n_points out of range");
+  if (!d->perm || !d->level_offset || !d->cl_start || !d->cl_end || !d->near_rowptr ||
+      !d->blr_rowptr || (d->blob_len > 0 && !d->blob))
+    return fail(H2G_ERR_BAD_EXPORT, "missing array");
+  if (d->level_offset[d->kappa + 1] != d->n_clusters)
+    return fail(H2G_ERR_BAD_EXPORT, "level_offset / n_clusters mismatch");
+  const int64_t lo_leaf = d->level_offset[d->kappa];
+  if (d->cl_start[lo_leaf] != 0 || d->cl_end[d->n_clusters - 1] != d->n_points)
+    return fail(H2G_ERR_BAD_EXPORT, "leaf slices do not tile [0, N)");
+  return H2G_OK;
+}
+
+// Check that an operator [off, off + rows*cols) lies in the blob.
+bool in_blob(const h2g_export_desc* d, int64_t off, int64_t rows, int64_t cols) {
+  return off >= 0 && rows >= 0 && cols >= 0 && off + rows * cols <= d->blob_len;
+}
+
+int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
+  const int kappa = d->kappa;
+  const int dim = d->dim;
+  const int64_t nc = d->n_clusters;
+  const int64_t* lo = d->level_offset;
+  const int64_t* st = d->cl_start;
+  const int64_t* en = d->cl_end;
+  auto nsz = [&](int64_t c) { return en[c] - st[c]; };
+  auto parent = [&](int64_t c, int l) { return lo[l - 1] + ((c - lo[l]) >> dim); };
+  auto level_of = [&](int64_t c) {
+    int l = 0;
+    while (l <= kappa && c >= lo[l + 1]) ++l;
+    return l;
+  };
+
+  // ---- arena layout (slots) ----
+  int64_t slots = 0;
+  p->q_tree = slots;
+  slots += d->n_points;
+  p->phi_tree = slots;
+  slots += d->n_points;
+  std::vector<std::vector<int64_t>> v_off(d->n_channels), u_off(d->n_channels);
+  for (int ch = 0; ch < d->n_channels; ++ch) {
+    const h2g_channel_desc& c = d->channels[ch];
+    if (!c.r_in || !c.r_out || !c.p2m_off || !c.l2p_off || !c.m2m_off || !c.l2l_off ||
+        !c.m2l_rowptr || (c.m2l_rowptr[nc] > 0 && (!c.m2l_src || !c.m2l_off)))
+      return fail(H2G_ERR_BAD_EXPORT, "channel array missing");
+    v_off[ch].resize(nc);
+    u_off[ch].resize(nc);
+    for (int64_t x = 0; x < nc; ++x) {
+      if (c.r_in[x] < 0 || c.r_out[x] < 0) return fail(H2G_ERR_BAD_EXPORT, "negative rank");
+      v_off[ch][x] = slots;
+      slots += c.r_out[x];
+    }
+    for (int64_t x = 0; x < nc; ++x) {
+      u_off[ch][x] = slots;
+      slots += c.r_in[x];
+    }
+  }
+  const int64_t blr_nnz = d->blr_rowptr[nc];
+  std::vector<int64_t> w_off(blr_nnz);
+  std::vector<int32_t> blr_x(blr_nnz);
+  for (int64_t x = 0; x < nc; ++x)
+    for (int64_t k = d->blr_rowptr[x]; k < d->blr_rowptr[x + 1]; ++k) blr_x[k] = (int32_t)x;
+  for (int64_t k = 0; k < blr_nnz; ++k) {
+    w_off[k] = slots;
+    slots += d->blr_rank[k];
+  }
+  // split-K partials of BLR stage 1
+  std::vector<int64_t> part_off(blr_nnz, -1);
+  std::vector<int32_t> n_chunks(blr_nnz, 1);
+  std::vector<int64_t> chunk_cols(blr_nnz, 0);
+  for (int64_t k = 0; k < blr_nnz; ++k) {
+    const int64_t pr = d->blr_rank[k];
+    const int64_t ny = nsz(d->blr_src[k]);
+    const int64_t cc = std::max<int64_t>(64, kBlrChunkDoubles / std::max<int64_t>(pr, 1));
+    chunk_cols[k] = cc;
+    const int64_t nch = (ny + cc - 1) / cc;
+    if (nch > 1) {
+      n_chunks[k] = (int32_t)nch;
+      part_off[k] = slots;
+      slots += nch * pr;
+    }
+  }
+  p->n_slots = slots;
+
+  // ---- up_leaf: P2M of every channel + BLR stage 1 (V^T q) ----
+  begin_phase(s, PH_GEMV, "up_leaf");
+  int64_t bytes = 0;
+  for (int64_t x = lo[kappa]; x < lo[kappa + 1]; ++x) {
+    for (int ch = 0; ch < d->n_channels; ++ch) {
+      const h2g_channel_desc& c = d->channels[ch];
+      if (c.p2m_off[x] < 0 || c.r_out[x] == 0) continue;
+      if (!in_blob(d, c.p2m_off[x], c.r_out[x], nsz(x)))
+        return fail(H2G_ERR_BAD_EXPORT, "p2m out of blob");
+      add_term(s, c.p2m_off[x], p->q_tree + st[x], c.r_out[x], nsz(x));
+      emit_task(s, v_off[ch][x], c.r_out[x], bytes);
+    }
+  }
+  std::vector<ReduceJob> jobs;
+  for (int64_t k = 0; k < blr_nnz; ++k) {
+    const int64_t y = d->blr_src[k];
+    const int64_t pr = d->blr_rank[k];
+    const int64_t ny = nsz(y);
+    if (pr <= 0) return fail(H2G_ERR_BAD_EXPORT, "BLR factor of rank 0 exported");
+    if (!in_blob(d, d->blr_v_off[k], ny, pr) || !in_blob(d, d->blr_u_off[k], nsz(blr_x[k]), pr))
+      return fail(H2G_ERR_BAD_EXPORT, "BLR factor out of blob");
+    if (n_chunks[k] == 1) {
+      add_term(s, d->blr_v_off[k], p->q_tree + st[y], pr, ny);
+      emit_task(s, w_off[k], pr, bytes);
+    } else {
+      const int64_t cc = chunk_cols[k];
+      for (int64_t ci = 0; ci < n_chunks[k]; ++ci) {
+        const int64_t c0 = ci * cc;
+        const int64_t ncols = std::min(cc, ny - c0);
+        add_term(s, d->blr_v_off[k] + c0 * pr, p->q_tree + st[y] + c0, pr, ncols);
+        emit_task(s, part_off[k] + ci * pr, pr, bytes);
+      }
+      ReduceJob j;
+      j.w_off = w_off[k];
+      j.part_off = part_off[k];
+      j.p = (int32_t)pr;
+      j.chunks = n_chunks[k];
+      jobs.push_back(j);
+    }
+  }
+  s.phases.back().alg_bytes = bytes;
+  end_phase(s);
+
+  if (!jobs.empty()) {
+    begin_phase(s, PH_REDUCE, "blr_reduce");
+    int64_t rb = 0;
+    for (const ReduceJob& j : jobs) {
+      s.jobs.push_back(j);
+      rb += 8LL * j.p * (j.chunks + 1);
+    }
+    s.phases.back().alg_bytes = 0;  // workspace traffic, not operator bytes
+    (void)rb;
+    end_phase(s);
+  }
+
+  // ---- upward: M2M levels kappa-1 .. 1 ----
+  for (int l = kappa - 1; l >= 1; --l) {
+    begin_phase(s, PH_GEMV, "m2m_l" + std::to_string(l));
+    bytes = 0;
+    for (int ch = 0; ch < d->n_channels; ++ch) {
+      const h2g_channel_desc& c = d->channels[ch];
+      for (int64_t x = lo[l]; x < lo[l + 1]; ++x) {
+        if (c.r_out[x] == 0) continue;
+        const int64_t c0 = lo[l + 1] + ((x - lo[l]) << dim);
+        for (int64_t cc = c0; cc < c0 + (1 << dim); ++cc) {
+          if (c.m2m_off[cc] < 0 || c.r_out[cc] == 0) continue;
+          if (!in_blob(d, c.m2m_off[cc], c.r_out[x], c.r_out[cc]))
+            return fail(H2G_ERR_BAD_EXPORT, "m2m out of blob");
+          add_term(s, c.m2m_off[cc], v_off[ch][cc], c.r_out[x], c.r_out[cc]);
+        }
+        emit_task(s, v_off[ch][x], c.r_out[x], bytes);
+      }
+    }
+    s.phases.back().alg_bytes = bytes;
+    end_phase(s);
+  }
+
+  // ---- downward: M2L (+ fused L2L) levels 1 .. kappa ----
+  for (int l = 1; l <= kappa; ++l) {
+    begin_phase(s, PH_GEMV, "down_l" + std::to_string(l));
+    bytes = 0;
+    for (int ch = 0; ch < d->n_channels; ++ch) {
+      const h2g_channel_desc& c = d->channels[ch];
+      for (int64_t x = lo[l]; x < lo[l + 1]; ++x) {
+        const int64_t ri = c.r_in[x];
+        if (ri == 0) continue;
+        for (int64_t k = c.m2l_rowptr[x]; k < c.m2l_rowptr[x + 1]; ++k) {
+          const int64_t y = c.m2l_src[k];
+          if (y < 0 || y >= nc || level_of(y) != l)
+            return fail(H2G_ERR_BAD_EXPORT, "m2l source not on the target's level");
+          if (c.r_out[y] == 0) continue;
+          if (!in_blob(d, c.m2l_off[k], ri, c.r_out[y]))
+            return fail(H2G_ERR_BAD_EXPORT, "m2l out of blob");
+          add_term(s, c.m2l_off[k], v_off[ch][y], ri, c.r_out[y]);
+        }
+        if (l >= 2) {
+          const int64_t px = parent(x, l);
+          if (c.l2l_off[x] >= 0 && c.r_in[px] > 0) {
+            if (!in_blob(d, c.l2l_off[x], ri, c.r_in[px]))
+              return fail(H2G_ERR_BAD_EXPORT, "l2l out of blob");
+            add_term(s, c.l2l_off[x], u_off[ch][px], ri, c.r_in[px]);
+          }
+        }
+        emit_task(s, u_off[ch][x], ri, bytes);
+      }
+    }
+    s.phases.back().alg_bytes = bytes;
+    end_phase(s);
+  }
+
+  // ---- leaf: L2P + BLR stage 2 + near -> phi_tree ----
+  begin_phase(s, PH_GEMV, "leaf");
+  bytes = 0;
+  for (int64_t x = lo[kappa]; x < lo[kappa + 1]; ++x) {
+    const int64_t nx = nsz(x);
+    if (nx == 0) continue;
+    for (int ch = 0; ch < d->n_channels; ++ch) {
+      const h2g_channel_desc& c = d->channels[ch];
+      if (c.l2p_off[x] < 0 || c.r_in[x] == 0) continue;
+      if (!in_blob(d, c.l2p_off[x], nx, c.r_in[x]))
+        return fail(H2G_ERR_BAD_EXPORT, "l2p out of blob");
+      add_term(s, c.l2p_off[x], u_off[ch][x], nx, c.r_in[x]);
+    }
+    // BLR stage 2: ancestors-or-self A at levels 1..kappa, rows of x inside U_AY
+    int64_t a = x;
+    for (int l = kappa; l >= 1; --l) {
+      for (int64_t k = d->blr_rowptr[a]; k < d->blr_rowptr[a + 1]; ++k)
+        add_term(s, d->blr_u_off[k] + (st[x] - st[a]), w_off[k], nsz(a), d->blr_rank[k]);
+      if (l > 1) a = parent(a, l);
+    }
+    for (int64_t k = d->near_rowptr[x]; k < d->near_rowptr[x + 1]; ++k) {
+      const int64_t y = d->near_src[k];
+      if (y < 0 || y >= nc) return fail(H2G_ERR_BAD_EXPORT, "near source out of range");
+      if (!in_blob(d, d->near_off[k], nx, nsz(y)))
+        return fail(H2G_ERR_BAD_EXPORT, "near block out of blob");
+      add_term(s, d->near_off[k], p->q_tree + st[y], nx, nsz(y));
+    }
+    emit_task(s, p->phi_tree + st[x], nx, bytes);
+  }
+  // BLR stage-2 bytes are counted per leaf above; stage-1 in up_leaf.
+  s.phases.back().alg_bytes = bytes;
+  end_phase(s);
+  (void)level_of;
+  return H2G_OK;
+}
+
+inline int grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 8));
+}
+
+int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s) {
+  const int64_t n = ph.task_end - ph.task_begin;
+  if (n <= 0) return H2G_OK;
+  if (ph.kind == PH_GEMV) {
+    gemv_tasks_kernel<<<(unsigned)n, kWarps * 32, 0, s>>>(p->d_tasks + ph.task_begin, p->d_terms,
+                                                          p->d_blob, p->d_arena);
+  } else {
+    reduce_partials_kernel<<<(unsigned)n, 128, 0, s>>>(p->d_jobs + ph.task_begin, (int)n,
+                                                       p->d_arena);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return H2G_OK;
+}
+
+int run_middle(h2g_plan* p, cudaStream_t s) {
+  if (p->graph_exec) {
+    CUDA_TRY(cudaGraphLaunch(p->graph_exec, s));
+    return H2G_OK;
+  }
+  for (const Phase& ph : p->phases) {
+    int rc = launch_phase(p, ph, s);
+    if (rc) return rc;
+  }
+  return H2G_OK;
+}
+
+int check_vec_args(h2g_plan* p, int64_t n, int64_t nrhs, int64_t ld) {
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  if (n != p->N) return fail(H2G_ERR_LENGTH_MISMATCH, "vector length mismatch");
+  if (nrhs < 1 || ld < nrhs) return fail(H2G_ERR_INVALID_ARG, "bad nrhs / ld");
+  return H2G_OK;
+}
+
+void free_plan(h2g_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  cudaFree(p->d_blob);
+  cudaFree(p->d_arena);
+  cudaFree(p->d_perm);
+  cudaFree(p->d_tasks);
+  cudaFree(p->d_terms);
+  cudaFree(p->d_jobs);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+}
+
+int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
+  int rc = validate(d);
+  if (rc) return rc;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(H2G_ERR_NO_DEVICE, "no CUDA device visible");
+  if (device < 0 || device >= ndev) return fail(H2G_ERR_NO_DEVICE, "device index out of range");
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(H2G_ERR_NO_DEVICE, std::string("device is not sm_100+: ") + prop.name);
+  CUDA_TRY(cudaSetDevice(device));
+
+  h2g_plan* p = new h2g_plan();
+  p->device = device;
+  p->N = d->n_points;
+  p->mem_scalars = d->mem_scalars;
+  HostSchedule s;
+  rc = build_schedule(d, p, s);
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  p->phases = s.phases;
+  p->n_tasks = (int64_t)s.tasks.size();
+  p->n_terms = (int64_t)s.terms.size();
+  if (p->n_terms >= (1LL << 31)) {
+    delete p;
+    return fail(H2G_ERR_BAD_EXPORT, "too many terms for int32 indexing");
+  }
+  std::vector<int32_t> perm32(p->N);
+  for (int64_t i = 0; i < p->N; ++i) {
+    if (d->perm[i] < 0 || d->perm[i] >= p->N) {
+      delete p;
+      return fail(H2G_ERR_BAD_EXPORT, "perm entry out of range");
+    }
+    perm32[i] = (int32_t)d->perm[i];
+  }
+  auto upload = [&](void** dst, const void* src, size_t bytes) -> int {
+    if (bytes == 0) return H2G_OK;
+    CUDA_TRY(cudaMalloc(dst, bytes));
+    CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+    return H2G_OK;
+  };
+  rc = [&]() -> int {
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->blob_len = d->blob_len;
+    int r;
+    if ((r = upload((void**)&p->d_blob, d->blob, sizeof(double) * d->blob_len))) return r;
+    if ((r = upload((void**)&p->d_perm, perm32.data(), sizeof(int32_t) * p->N))) return r;
+    if ((r = upload((void**)&p->d_tasks, s.tasks.data(), sizeof(Task) * s.tasks.size()))) return r;
+    if ((r = upload((void**)&p->d_terms, s.terms.data(), sizeof(Term) * s.terms.size()))) return r;
+    if ((r = upload((void**)&p->d_jobs, s.jobs.data(), sizeof(ReduceJob) * s.jobs.size()))) return r;
+    CUDA_TRY(cudaMalloc((void**)&p->d_arena, sizeof(double) * p->n_slots));
+    CUDA_TRY(cudaMemset(p->d_arena, 0, sizeof(double) * p->n_slots));
+    p->workspace_bytes = sizeof(double) * p->n_slots + sizeof(Task) * s.tasks.size() +
+                         sizeof(Term) * s.terms.size() + sizeof(ReduceJob) * s.jobs.size() +
+                         sizeof(int32_t) * p->N;
+    // capture the fixed middle phases into one CUDA graph
+    CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+    for (const Phase& ph : p->phases) {
+      int lr = launch_phase(p, ph, p->stream);
+      if (lr) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(p->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        return lr;
+      }
+    }
+    CUDA_TRY(cudaStreamEndCapture(p->stream, &p->graph));
+    CUDA_TRY(cudaGraphInstantiate(&p->graph_exec, p->graph, 0));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    return H2G_OK;
+  }();
+  if (rc) {
+    std::string keep = g_detail;
+    free_plan(p);
+    g_detail = keep;
+    return rc;
+  }
+  *out = p;
+  return H2G_OK;
+}
+
+int matvec_impl(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nrhs, int64_t ld,
+                cudaStream_t s) {
+  int rc = check_vec_args(p, n, nrhs, ld);
+  if (rc) return rc;
+  if (!q || !phi) return fail(H2G_ERR_INVALID_ARG, "null vector");
+  CUDA_TRY(cudaSetDevice(p->device));
+  for (int64_t j = 0; j < nrhs; ++j) {
+    gather_perm_kernel<<<grid_for(n), 256, 0, s>>>(q + j, ld, p->d_perm, p->d_arena + p->q_tree, n);
+    CUDA_TRY(cudaGetLastError());
+    rc = run_middle(p, s);
+    if (rc) return rc;
+    scatter_perm_kernel<<<grid_for(n), 256, 0, s>>>(p->d_arena + p->phi_tree, p->d_perm, phi + j,
+                                                    ld, n);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return H2G_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int h2g_abi_version(void) { return H2G_ABI_VERSION; }
+
+const char* h2g_error_string(int code) {
+  switch (code) {
+    case H2G_OK: return "ok";
+    case H2G_ERR_LENGTH_MISMATCH: return "vector length mismatch";
+    case H2G_ERR_BAD_EXPORT: return "bad export";
+    case H2G_ERR_CUDA: return "CUDA error";
+    case H2G_ERR_NO_DEVICE: return "no usable sm_100 CUDA device";
+    case H2G_ERR_INVALID_ARG: return "invalid argument";
+    case H2G_ERR_OOM: return "out of device memory";
+    default: return "unknown error";
+  }
+}
+
+const char* h2g_last_error_detail(void) { return g_detail.c_str(); }
+
+int h2g_plan_create(const h2g_export_desc* desc, int device, h2g_plan** out) {
+  if (!out) return fail(H2G_ERR_INVALID_ARG, "null out");
+  *out = nullptr;
+  return create_impl(desc, device, out);
+}
+
+int h2g_plan_destroy(h2g_plan* plan) {
+  free_plan(plan);
+  return H2G_OK;
+}
+
+int h2g_plan_get_stats(const h2g_plan* p, h2g_plan_stats* o) {
+  if (!p || !o) return fail(H2G_ERR_INVALID_ARG, "null argument");
+  o->n_points = p->N;
+  o->mem_scalars = p->mem_scalars;
+  o->alg_bytes = 8 * p->mem_scalars + 16 * p->N;
+  o->blob_bytes = 8 * p->blob_len;
+  o->workspace_bytes = p->workspace_bytes;
+  o->n_phases = (int32_t)p->phases.size();
+  o->n_launches = h2g_launches_per_matvec(p, 1);
+  o->n_tasks = p->n_tasks;
+  o->n_terms = p->n_terms;
+  o->device = p->device;
+  o->graph = p->graph_exec ? 1 : 0;
+  return H2G_OK;
+}
+
+int h2g_launches_per_matvec(const h2g_plan* p, int64_t nrhs) {
+  if (!p) return 0;
+  return (int)((p->phases.size() + 2) * (nrhs < 1 ? 1 : nrhs));
+}
+
+int h2g_matvec(h2g_plan* plan, const double* q_dev, double* phi_dev, int64_t n, int64_t nrhs,
+               int64_t ld, void* stream) {
+  return matvec_impl(plan, q_dev, phi_dev, n, nrhs, ld, (cudaStream_t)stream);
+}
+
+int h2g_matvec_host(h2g_plan* p, const double* q_host, double* phi_host, int64_t n, int64_t nrhs,
+                    int64_t ld) {
+  int rc = check_vec_args(p, n, nrhs, ld);
+  if (rc) return rc;
+  if (!q_host || !phi_host) return fail(H2G_ERR_INVALID_ARG, "null vector");
+  CUDA_TRY(cudaSetDevice(p->device));
+  const size_t bytes = sizeof(double) * (size_t)n * (size_t)ld;
+  double *dq = nullptr, *dphi = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&dq, bytes, p->stream));
+  CUDA_TRY(cudaMallocAsync((void**)&dphi, bytes, p->stream));
+  CUDA_TRY(cudaMemcpyAsync(dq, q_host, bytes, cudaMemcpyHostToDevice, p->stream));
+  if (ld != nrhs)  // keep the caller's padding columns intact
+    CUDA_TRY(cudaMemcpyAsync(dphi, phi_host, bytes, cudaMemcpyHostToDevice, p->stream));
+  rc = matvec_impl(p, dq, dphi, n, nrhs, ld, p->stream);
+  if (rc == H2G_OK)
+    CUDA_TRY(cudaMemcpyAsync(phi_host, dphi, bytes, cudaMemcpyDeviceToHost, p->stream));
+  cudaFreeAsync(dq, p->stream);
+  cudaFreeAsync(dphi, p->stream);
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return rc;
+}
+
+int h2g_profile_phases(h2g_plan* p, const double* q_dev, double* phi_dev, int iters, double* ms,
+                       int64_t* bytes, const char** names, int cap, int* n_out) {
+  if (!p || !q_dev || !phi_dev || iters < 1) return fail(H2G_ERR_INVALID_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(p->device));
+  const int nph = (int)p->phases.size() + 2;  // + gather + scatter
+  std::vector<cudaEvent_t> ev(nph + 1);
+  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+  std::vector<double> acc(nph, 0.0);
+  cudaStream_t s = p->stream;
+  CUDA_TRY(cudaDeviceSynchronize());  // inputs may come from another stream
+  for (int it = 0; it < iters; ++it) {
+    CUDA_TRY(cudaEventRecord(ev[0], s));
+    gather_perm_kernel<<<grid_for(p->N), 256, 0, s>>>(q_dev, 1, p->d_perm, p->d_arena + p->q_tree,
+                                                       p->N);
+    CUDA_TRY(cudaEventRecord(ev[1], s));
+    for (size_t i = 0; i < p->phases.size(); ++i) {
+      int rc = launch_phase(p, p->phases[i], s);
+      if (rc) return rc;
+      CUDA_TRY(cudaEventRecord(ev[2 + i], s));
+    }
+    scatter_perm_kernel<<<grid_for(p->N), 256, 0, s>>>(p->d_arena + p->phi_tree, p->d_perm,
+                                                        phi_dev, 1, p->N);
+    CUDA_TRY(cudaEventRecord(ev[nph], s));
+    CUDA_TRY(cudaEventSynchronize(ev[nph]));
+    for (int i = 0; i < nph; ++i) {
+      float t = 0;
+      CUDA_TRY(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+      acc[i] += t;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  const int n = std::min(cap, nph);
+  for (int i = 0; i < n; ++i) {
+    ms[i] = acc[i] / iters;
+    if (i == 0) {
+      bytes[i] = 12 * p->N;  // q read (8) + perm (4); q_tree write counted in consumers
+      names[i] = "gather";
+    } else if (i == nph - 1) {
+      bytes[i] = 12 * p->N;
+      names[i] = "scatter";
+    } else {
+      bytes[i] = p->phases[i - 1].alg_bytes;
+      names[i] = p->phases[i - 1].name.c_str();
+    }
+  }
+  *n_out = n;
+  return H2G_OK;
+}
+
+}  // extern "C"

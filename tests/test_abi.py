@@ -1,0 +1,75 @@
+"""CPU-side checks of the C-ABI boundary: the library builds/loads, exports
+every symbol include/h2g.h declares, and fails loudly without a GPU."""
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2309_14085_b200 import _lib
+from paper_2309_14085_b200.build import build
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def _declared(header):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(h2g_[a-z_]+)\s*\(", src)))
+
+
+def test_build_and_load():
+    build(verbose=False)
+    L = _lib.load()
+    assert L.h2g_abi_version() == _lib.H2G_ABI_VERSION
+
+
+def test_every_declared_symbol_is_exported():
+    L = _lib.load()
+    declared = _declared("h2g.h")
+    assert set(declared) == set(_lib.H2G_SYMBOLS)
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def test_error_strings():
+    L = _lib.load()
+    assert L.h2g_error_string(1) == b"vector length mismatch"
+    assert L.h2g_error_string(0) == b"ok"
+
+
+def test_bad_descriptor_rejected_without_gpu():
+    L = _lib.load()
+    d = _lib.ExportDesc()
+    d.abi_version = 999
+    plan = C.c_void_p()
+    rc = L.h2g_plan_create(C.byref(d), 0, C.byref(plan))
+    assert rc == 2 and not plan.value
+    with pytest.raises(RuntimeError, match="bad export"):
+        _lib.check(rc)
+
+
+def test_struct_layout_matches_header():
+    # 4 int32 + 3 int64 + 4 pointers + 2 channel descs (9 pointers each) + 8 ptrs + len + ptr
+    assert C.sizeof(_lib.ChannelDesc) == 9 * 8
+    assert C.sizeof(_lib.ExportDesc) == 16 + 24 + 32 + 2 * 72 + 8 * 8 + 8 + 8
+
+
+def test_length_mismatch_maps_to_value_error():
+    with pytest.raises(ValueError, match="vector length mismatch"):
+        _lib.check(_lib.H2G_ERR_LENGTH_MISMATCH)
+
+
+def test_no_device_is_loud():
+    """Without a GPU the product path raises instead of falling back."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from golden_io import golden_names, load_golden
+    from paper_2309_14085_b200.gpu_rep import GpuHierRep
+    op, _, _ = load_golden(golden_names()[0])
+    with pytest.raises(RuntimeError, match="no usable sm_100 CUDA device|CUDA"):
+        GpuHierRep(op)
+    assert np.isfinite(op.blob).all()
