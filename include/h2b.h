@@ -1,0 +1,79 @@
+/*
+ * h2b.h — C ABI of the native (C++/OpenMP) operator builder.
+ *
+ * Restates the reference's construction of the H2* / (H2+H)* operators so
+ * that operators at the benchmark sizes can be built on the GPU box itself
+ * (the reference's Python build takes ~20-30 min at N=1M and cannot run
+ * there).  Output is the packed export consumed by h2g_plan_create
+ * (include/h2g.h).  Reference interfaces restated:
+ *
+ *   build_tree(particles, n_max)              tree.py:111-185
+ *   build_partition(tree, WeakVertex())       partition.py:77-137
+ *   Kernel.block(rows, cols) (+ Log2D,        kernels.py:36-57, 63-81
+ *     InverseR, Gaussian via the _f hook)
+ *   aca / aca_pivots / aca_factor             lowrank.py:69-159
+ *   solve_square / rsolve (LU, singular test) lowrank.py:162-180
+ *   _pivot_pair (retry at eps/10)             engine.py:39-51
+ *   select_pivots_b2t / select_pivots_t2b     engine.py:54-114
+ *   build_operators                           engine.py:133-187
+ *   build_blr(lists="ver", include_near=0)    blr.py:46-69
+ *   _attach_near(store_near=True)             engine.py:309-318
+ *   build_variant("h2star-bt"|"h2plusH-star") engine.py:325-373
+ */
+#ifndef H2B_H
+#define H2B_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define H2B_ABI_VERSION 1
+
+enum { H2B_VARIANT_H2STAR_BT = 0, H2B_VARIANT_H2PLUSH_STAR = 1 };
+enum { H2B_KERNEL_LOG2D = 0, H2B_KERNEL_LAP3D = 1, H2B_KERNEL_GAUSSIAN = 2 };
+enum { H2B_OK = 0, H2B_ERR_INVALID_ARG = 1, H2B_ERR_SINGULAR = 2, H2B_ERR_OOM = 3 };
+
+typedef struct h2b_params {
+  int32_t abi_version;   /* H2B_ABI_VERSION */
+  int32_t dim;           /* 1..3 */
+  int64_t n_points;
+  const double* points;  /* n_points x dim, row-major, original order */
+  int32_t n_max;         /* leaf size (tree.py:111) */
+  int32_t variant;       /* H2B_VARIANT_* */
+  int32_t kernel;        /* H2B_KERNEL_* */
+  int32_t has_diag;      /* Kernel.diag is not None */
+  double zero_value;     /* Kernel.zero_value (r == 0, i != j) */
+  double diag;           /* Kernel.diag */
+  double shift;          /* Kernel.shift (added on i == j) */
+  double sigma;          /* Gaussian width */
+  double eps_far;        /* NCA tolerance of the far channel */
+  double eps_ver;        /* NCA / ACA tolerance of the vertex leg */
+  int32_t n_threads;     /* 0 = OpenMP default */
+  int32_t reserved;
+} h2b_params;
+
+typedef struct h2b_result h2b_result;
+
+/* dtype codes for h2b_get_array */
+enum { H2B_I32 = 0, H2B_I64 = 1, H2B_F64 = 2 };
+
+int h2b_build(const h2b_params* params, h2b_result** out);
+/* Named arrays of the packed export (packed.py field names, channel fields
+ * prefixed "ch0_"/"ch1_").  The pointer stays valid until h2b_free. */
+int h2b_get_array(const h2b_result* r, const char* name, const void** ptr, int64_t* len,
+                  int32_t* dtype);
+/* Scalars: "kappa", "n_channels", "mem_scalars", "n_clusters". */
+int64_t h2b_get_scalar(const h2b_result* r, const char* name);
+/* Wall-clock seconds of the build stages: "tree", "partition", "pivots",
+ * "operators", "blr", "near", "total". */
+double h2b_get_timing(const h2b_result* r, const char* name);
+void h2b_free(h2b_result* r);
+const char* h2b_last_error(void);
+int h2b_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2B_H */

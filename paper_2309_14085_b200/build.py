@@ -2,7 +2,8 @@
 
     python -m paper_2309_14085_b200.build
 
-produces ``paper_2309_14085_b200/lib/libh2g.so`` (CUDA matvec, include/h2g.h).
+produces ``paper_2309_14085_b200/lib/libh2g.so`` (CUDA matvec, include/h2g.h)
+and ``libh2b.so`` (native C++/OpenMP operator builder, include/h2b.h).
 The .so files are git-ignored but travel to the GPU box with the snapshot.
 """
 
@@ -23,8 +24,14 @@ NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
            "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 
 TARGETS = {
-    "libh2g.so": (["h2g_plan.cu"], ["h2g_kernels.cuh"]),
+    "libh2g.so": (["h2g_plan.cu"], ["h2g_kernels.cuh", "h2g_stream.cuh"], "h2g.h"),
+    "libh2b.so": (["h2b_build.cpp"], [], "h2b.h"),
 }
+CXX = os.environ.get("H2_CXX", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++")
+# no -march=native / -ffast-math: keep IEEE fp64 operation order (no FMA
+# contraction) like numpy's separate ufunc passes in the reference ACA
+CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
+            "-I", os.path.join(ROOT, "include")]
 
 
 def _stale(out, srcs):
@@ -37,13 +44,16 @@ def _stale(out, srcs):
 def build(force: bool = False, verbose: bool = True) -> dict:
     os.makedirs(LIBDIR, exist_ok=True)
     built = {}
-    for name, (srcs, deps) in TARGETS.items():
+    for name, (srcs, deps, header) in TARGETS.items():
         out = os.path.join(LIBDIR, name)
         src_paths = [os.path.join(CSRC, s) for s in srcs]
         dep_paths = src_paths + [os.path.join(CSRC, s) for s in deps] + [
-            os.path.join(ROOT, "include", "h2g.h")]
+            os.path.join(ROOT, "include", header), __file__]
         if force or _stale(out, dep_paths):
-            cmd = [NVCC, *ARCH, *NVFLAGS, "-shared", "-o", out, *src_paths]
+            if srcs[0].endswith(".cu"):
+                cmd = [NVCC, *ARCH, *NVFLAGS, "-shared", "-o", out, *src_paths]
+            else:
+                cmd = [CXX, *CXXFLAGS, "-shared", "-o", out, *src_paths]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.run(cmd, check=True)

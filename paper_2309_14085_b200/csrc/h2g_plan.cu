@@ -25,12 +25,14 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/h2g.h"
 #include "h2g_kernels.cuh"
+#include "h2g_stream.cuh"
 
 using namespace h2g;
 
@@ -58,6 +60,8 @@ struct Phase {
   std::string name;
   int64_t task_begin = 0, task_end = 0;  // into d_tasks (GEMV) or d_jobs (REDUCE)
   int64_t alg_bytes = 0;                 // operator + vector bytes (algorithmic)
+  int64_t cta_off = 0;                   // streaming engine: CTA ranges at d_cta[cta_off ..]
+  int32_t n_cta = 0;
 };
 
 struct HostSchedule {
@@ -89,6 +93,12 @@ struct h2g_plan {
   ReduceJob* d_jobs = nullptr;
   std::vector<Phase> phases;
   int64_t n_tasks = 0, n_terms = 0;
+  Chunk* d_chunks = nullptr;
+  Seg* d_segs = nullptr;
+  int64_t* d_cta = nullptr;
+  int64_t n_chunks = 0;
+  int engine = 1;  // 1 = TMA-bulk streaming engine, 0 = direct-load task kernel
+  int n_sm = 148;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   int64_t workspace_bytes = 0;
@@ -380,6 +390,102 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
   return H2G_OK;
 }
 
+// Cut every task of every GEMV phase into streaming chunks and partition
+// whole tasks over at most n_sm persistent CTAs, balanced by bytes.  Terms of
+// a task whose operator data is contiguous in the blob (lda == m and the next
+// term starts where the previous ends, e.g. the M2L row of one target or the
+// near blocks of one leaf) share chunks, one x segment per term.
+void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
+                  std::vector<Chunk>& chunks, std::vector<Seg>& segs, std::vector<int64_t>& cta) {
+  for (Phase& ph : phases) {
+    if (ph.kind != PH_GEMV) continue;
+    const int64_t nt = ph.task_end - ph.task_begin;
+    std::vector<int64_t> task_chunk0(nt + 1);
+    std::vector<double> task_cost(nt);
+    double total = 0;
+    for (int64_t ti = 0; ti < nt; ++ti) {
+      const Task& t = s.tasks[ph.task_begin + ti];
+      task_chunk0[ti] = (int64_t)chunks.size();
+      double cost = 0;
+      bool open = false;        // current chunk accepts contiguous continuation
+      int64_t a_end = -1;       // blob offset right after the current chunk's data
+      int64_t per_open = 0;     // column capacity of the current chunk
+      for (int32_t k = t.t_begin; k < t.t_end; ++k) {
+        const Term& tm = s.terms[k];
+        const bool strided = tm.lda != t.m;
+        const int64_t ldas = strided ? ((t.m + 1) & ~1) + 2 : t.m;
+        const int64_t per = std::max<int64_t>(
+            1, std::min<int64_t>(kChunkCols, kChunkA / std::max<int64_t>(ldas, 1)));
+        int64_t c0 = 0;
+        while (c0 < tm.ncols) {
+          const int64_t a_here = tm.a_off + c0 * tm.lda;
+          int64_t take;
+          if (open && !strided && a_here == a_end && chunks.back().n_seg < kMaxSeg &&
+              chunks.back().ncols < per_open) {
+            take = std::min<int64_t>(tm.ncols - c0, per_open - chunks.back().ncols);
+            Seg sg{tm.x_off + c0, (int32_t)take, 0};
+            segs.push_back(sg);
+            chunks.back().n_seg += 1;
+            chunks.back().ncols += (int32_t)take;
+          } else {
+            take = std::min<int64_t>(tm.ncols - c0, per);
+            Chunk c;
+            c.a_off = a_here;
+            c.y_off = t.y_off;
+            c.lda = tm.lda;
+            c.m = t.m;
+            c.ncols = (int32_t)take;
+            c.flags = 0;
+            c.seg_begin = (int32_t)segs.size();
+            c.n_seg = 1;
+            segs.push_back(Seg{tm.x_off + c0, (int32_t)take, 0});
+            chunks.push_back(c);
+            cost += 1024.0;
+            open = !strided;
+            per_open = per;
+          }
+          cost += 8.0 * t.m * take;
+          a_end = a_here + t.m * take;
+          c0 += take;
+        }
+        if (strided) open = false;
+      }
+      if ((int64_t)chunks.size() == task_chunk0[ti]) {  // no terms: writes zeros
+        Chunk c{};
+        c.y_off = t.y_off;
+        c.lda = t.m;
+        c.m = t.m;
+        c.seg_begin = (int32_t)segs.size();
+        c.n_seg = 0;
+        chunks.push_back(c);
+        cost += 1024.0;
+      }
+      chunks.back().flags |= kLastOfTask;
+      task_cost[ti] = cost;
+      total += cost;
+    }
+    task_chunk0[nt] = (int64_t)chunks.size();
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(nt, n_sm));
+    ph.cta_off = (int64_t)cta.size();
+    cta.push_back(task_chunk0[0]);
+    double acc = 0;
+    int64_t g = 0;
+    for (int64_t ti = 0; ti < nt; ++ti) {
+      acc += task_cost[ti];
+      const int64_t left_tasks = nt - ti - 1;
+      const int64_t left_groups = G - g - 1;
+      const bool cut = left_groups > 0 && left_tasks >= 1 &&
+                       (acc >= total * (double)(g + 1) / (double)G || left_tasks <= left_groups);
+      if (cut) {
+        cta.push_back(task_chunk0[ti + 1]);
+        ++g;
+      }
+    }
+    cta.push_back(task_chunk0[nt]);
+    ph.n_cta = (int32_t)(cta.size() - ph.cta_off - 1);
+  }
+}
+
 inline int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 8));
@@ -388,7 +494,10 @@ inline int grid_for(int64_t n) {
 int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s) {
   const int64_t n = ph.task_end - ph.task_begin;
   if (n <= 0) return H2G_OK;
-  if (ph.kind == PH_GEMV) {
+  if (ph.kind == PH_GEMV && p->engine == 1) {
+    stream_gemv_kernel<<<ph.n_cta, kStreamThreads, kStreamSmem, s>>>(
+        p->d_chunks, p->d_segs, p->d_cta + ph.cta_off, p->d_blob, p->d_arena);
+  } else if (ph.kind == PH_GEMV) {
     gemv_tasks_kernel<<<(unsigned)n, kWarps * 32, 0, s>>>(p->d_tasks + ph.task_begin, p->d_terms,
                                                           p->d_blob, p->d_arena);
   } else {
@@ -429,6 +538,9 @@ void free_plan(h2g_plan* p) {
   cudaFree(p->d_tasks);
   cudaFree(p->d_terms);
   cudaFree(p->d_jobs);
+  cudaFree(p->d_chunks);
+  cudaFree(p->d_segs);
+  cudaFree(p->d_cta);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -456,6 +568,19 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
     delete p;
     return rc;
   }
+  {
+    const char* e = getenv("H2G_ENGINE");
+    if (e && std::string(e) == "ldg") p->engine = 0;
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess &&
+        nsm > 0)
+      p->n_sm = nsm;
+  }
+  std::vector<Chunk> chunks;
+  std::vector<int64_t> cta;
+  std::vector<Seg> segs;
+  build_chunks(s, s.phases, p->n_sm, chunks, segs, cta);
+  p->n_chunks = (int64_t)chunks.size();
   p->phases = s.phases;
   p->n_tasks = (int64_t)s.tasks.size();
   p->n_terms = (int64_t)s.terms.size();
@@ -486,10 +611,18 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
     if ((r = upload((void**)&p->d_tasks, s.tasks.data(), sizeof(Task) * s.tasks.size()))) return r;
     if ((r = upload((void**)&p->d_terms, s.terms.data(), sizeof(Term) * s.terms.size()))) return r;
     if ((r = upload((void**)&p->d_jobs, s.jobs.data(), sizeof(ReduceJob) * s.jobs.size()))) return r;
-    CUDA_TRY(cudaMalloc((void**)&p->d_arena, sizeof(double) * p->n_slots));
-    CUDA_TRY(cudaMemset(p->d_arena, 0, sizeof(double) * p->n_slots));
+    if ((r = upload((void**)&p->d_chunks, chunks.data(), sizeof(Chunk) * chunks.size()))) return r;
+    if ((r = upload((void**)&p->d_cta, cta.data(), sizeof(int64_t) * cta.size()))) return r;
+    if ((r = upload((void**)&p->d_segs, segs.data(), sizeof(Seg) * segs.size()))) return r;
+    CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kStreamSmem));
+    // +8 slots of slack: aligned bulk copies of x may read up to 8 bytes past a slice
+    CUDA_TRY(cudaMalloc((void**)&p->d_arena, sizeof(double) * (p->n_slots + 8)));
+    CUDA_TRY(cudaMemset(p->d_arena, 0, sizeof(double) * (p->n_slots + 8)));
     p->workspace_bytes = sizeof(double) * p->n_slots + sizeof(Task) * s.tasks.size() +
                          sizeof(Term) * s.terms.size() + sizeof(ReduceJob) * s.jobs.size() +
+                         sizeof(Chunk) * chunks.size() + sizeof(int64_t) * cta.size() +
+                         sizeof(Seg) * segs.size() +
                          sizeof(int32_t) * p->N;
     // capture the fixed middle phases into one CUDA graph
     CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));

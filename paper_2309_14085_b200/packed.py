@@ -39,7 +39,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 SCHEMA = "h2g-export-1"
-ALIGN = 4  # doubles: 32-byte sector alignment of every matrix start
+ALIGN = 1  # doubles: blocks are packed back to back (TMA bulk copies align down on device)
 
 CHANNEL_FIELDS = ("r_in", "r_out", "p2m_off", "l2p_off", "m2m_off", "l2l_off",
                   "m2l_rowptr", "m2l_src", "m2l_off")
