@@ -1,0 +1,318 @@
+"""Benchmark: H2* / (H2+H)* matvec on B200 (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2] [--variants h2star-bt,h2plusH-star]
+
+Workload (configs[1]): 2D, N = 1,048,576 points i.i.d. uniform in [-1,1]^2
+(seed 42, reference bench.py:41), K(x,y) = log|x-y| (Log2D, kernels.py:63-71),
+quadtree leaf <= 64, NCA tolerance 1e-8, single RHS q ~ N(0,1) (seed 43).  The
+operator is built on the box by the native builder (libh2b.so), which
+restates the reference construction (identical ranks/pivots on every golden
+case); the reference's own Python build is infeasible here (~30 min).
+
+A step is one matvec phi = K~ q.  ``value`` = matvecs/s of the headline
+variant (h2star-bt) over all ranks, device-timed with CUDA events on the
+plan's stream, inputs resident in HBM; the operator (6.6 GB) is far larger
+than L2 (126 MB), so no flush is needed.  ``e2e`` is the same metric through
+the public API (GpuHierRep.matvec on a pinned host vector: H2D copy, matvec,
+D2H copy inside the timed region).  ``roofline`` reports the streaming GEMV
+kernel's achieved algorithmic bytes/s against MEASURED_PEAKS.json.
+``cpu_baseline`` times the oracle port of the reference matvec
+(oracle/packed_matvec.py, one core) on a bounded sample.
+
+--impl reference times that CPU port as the reference arm (rank 0 only).
+Multi-GPU (N > 1): interim "replicas" mode -- every rank runs the full
+operator (weak scaling); the subtree-sharded path is DESIGN.md's next row.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+# the CPU reference leg is a single interpreter thread issuing small GEMVs
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(N=4096, d=2, kernel="log2d", n_max=64, eps=1e-8,
+                 desc="cfg1: 2D N=4096 uniform [-1,1]^2, log r, leaf<=64, eps 1e-8"),
+    "cfg2": dict(N=1048576, d=2, kernel="log2d", n_max=64, eps=1e-8,
+                 desc="cfg2: 2D N=1048576 uniform [-1,1]^2, log r, leaf<=64, eps 1e-8"),
+    "cfg3": dict(N=1048576, d=3, kernel="lap3d", n_max=64, eps=1e-6,
+                 desc="cfg3: 3D N=1048576 uniform [-1,1]^3, 1/r, leaf<=64, eps 1e-6"),
+}
+METRIC = "H2* matvec/s (fp64) on 1 B200, 2D N=1M log r eps 1e-8"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def build_op(cfg, variant, n_threads=0):
+    from paper_2309_14085_b200.builder import build_variant, uniform_points
+    pts = uniform_points(cfg["N"], cfg["d"], 42)
+    t0 = time.perf_counter()
+    op = build_variant(variant, pts, cfg["kernel"], cfg["n_max"], cfg["eps"], n_threads=n_threads)
+    return op, time.perf_counter() - t0
+
+
+def cpu_port_time(op, q, budget_s=15.0, max_steps=20):
+    """Oracle port of HierRep.matvec (engine.py:250-269), one core."""
+    from oracle.packed_matvec import packed_matvec
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_steps and (time.perf_counter() - t_start) < budget_s:
+        t0 = time.perf_counter()
+        packed_matvec(op, q)
+        times.append(time.perf_counter() - t0)
+    return float(np.mean(times)), len(times)
+
+
+def bench_variant(op, args, torch, dev, rank, world):
+    from paper_2309_14085_b200.gpu_rep import GpuHierRep
+    rep = GpuHierRep(op, device=dev)
+    N = op.N
+    q = np.random.default_rng(43).standard_normal(N)
+    qd = torch.from_numpy(q).to(f"cuda:{dev}")
+    out = torch.empty_like(qd)
+    stream = torch.cuda.Stream(device=dev)
+    L, plan = rep._L, rep._plan
+
+    def step():
+        L.h2g_matvec(plan, qd.data_ptr(), out.data_ptr(), N, 1, 1, stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    # per-phase CUDA-event timing on the plan stream (roofline of the GEMV kernel)
+    prof = rep.profile_phases(qd, out, iters=max(3, min(args.steps, 10)))
+    # e2e through the public API with pinned host buffers
+    q_pin = torch.from_numpy(q).pin_memory()
+    qh = q_pin.numpy()
+    phi = None
+    for _ in range(max(1, args.warmup // 2)):
+        phi = rep.matvec(qh)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        phi = rep.matvec(qh)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    res = {"rep": rep, "ms": ms, "prof": prof, "clk": clk.summary(), "e2e_s": e2e_s,
+           "q": q, "phi": phi, "out": out}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--variants", default="h2star-bt,h2plusH-star")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = CONFIGS[args.config]
+    variants = [v for v in args.variants.split(",") if v]
+    rank, world, local = dist_env()
+    n_threads = max(1, (os.cpu_count() or 1) // max(1, world))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        op, tb = build_op(cfg, variants[0], n_threads=os.cpu_count() or 1)
+        q = np.random.default_rng(43).standard_normal(cfg["N"])
+        from oracle.packed_matvec import packed_matvec
+        for _ in range(min(args.warmup, 1)):
+            packed_matvec(op, q)
+        budget = 240.0
+        times = []
+        t_all = time.perf_counter()
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            packed_matvec(op, q)
+            times.append(time.perf_counter() - t0)
+            if time.perf_counter() - t_all > budget:
+                break
+        s = float(np.mean(times))
+        v = 1.0 / s
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "matvec/s",
+                "n_gpus": args.gpus, "steps": len(times), "warmup": min(args.warmup, 1),
+                "ms_per_step": s * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": cfg["desc"], "variant": variants[0], "N": cfg["N"],
+                           "mem_scalars": int(op.mem_scalars),
+                           "operator": "native build (libh2b.so), identical structure/ranks "
+                                       "to the reference build"},
+                "cpu_baseline": {"value": v, "unit": "matvec/s", "cores": 1, "kind": "port",
+                                 "sample": f"{len(times)} full matvecs of the oracle port "
+                                           "(oracle/packed_matvec.py: reference loop structure, "
+                                           "numpy @ per block, OPENBLAS_NUM_THREADS=1)"},
+                "e2e": {"value": v, "unit": "matvec/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    if world > 1:
+        torch.distributed.init_process_group("nccl")
+    dev = local if torch.cuda.device_count() > local else 0
+    torch.cuda.set_device(dev)
+
+    results = {}
+    for v in variants:
+        op, tb = build_op(cfg, v, n_threads=n_threads)
+        r = bench_variant(op, args, torch, dev, rank, world)
+        r["op"] = op
+        r["build_s"] = tb
+        results[v] = r
+        if v != variants[0]:
+            r["rep"].close()
+
+    head = variants[0]
+    R = results[head]
+    op, rep = R["op"], R["rep"]
+    mvps = 1e3 / R["ms"]
+    value = mvps * world
+    # roofline: streaming GEMV kernel phases (algorithmic bytes / event time)
+    gemv = [p for p in R["prof"] if p["phase"] not in ("gather", "scatter", "blr_reduce")]
+    k_bytes = sum(p["bytes"] for p in gemv)
+    k_ms = sum(p["ms"] for p in gemv)
+    peak, peak_src = _peaks()
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    dom = max(gemv, key=lambda p: p["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{head}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": R["ms"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (uniform_points seed 42, q ~ N(0,1) seed 43)",
+        "config": {"workload": cfg["desc"], "variant": head, "N": op.N, "kappa": op.kappa,
+                   "mem_scalars": int(op.mem_scalars), "alg_bytes": rep.alg_bytes,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "operator > L2 (no flush)", "build_s": round(R["build_s"], 2)},
+        "achieved_GBps": rep.alg_bytes / (R["ms"] * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "stream_gemv_kernel (all GEMV phases)",
+                     "dominant_phase": {"name": dom["phase"], "ms": dom["ms"],
+                                        "GBps": dom["bytes"] / (dom["ms"] * 1e-3) / 1e9}},
+        "e2e": {"value": world / R["e2e_s"], "unit": "matvec/s",
+                "h2d_bytes_per_step": 8 * op.N, "d2h_bytes_per_step": 8 * op.N},
+        "gpu_launches": args.steps * rep.launches_per_matvec(),
+        "clocks": R["clk"],
+        "phases_us": {p["phase"]: round(p["ms"] * 1e3, 1) for p in R["prof"]},
+    }
+    others = {}
+    for v in variants[1:]:
+        r = results[v]
+        others[v] = {"ms_per_step": r["ms"], "matvec_per_s": 1e3 / r["ms"] * world,
+                     "mem_scalars": int(r["op"].mem_scalars),
+                     "achieved_GBps": (8 * r["op"].mem_scalars + 16 * r["op"].N) / (r["ms"] * 1e-3) / 1e9,
+                     "e2e_matvec_per_s": world / r["e2e_s"], "build_s": round(r["build_s"], 2)}
+    if others:
+        line["variants"] = others
+    if rank == 0 and world == 1:
+        t_cpu, n_cpu = cpu_port_time(op, R["q"], budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": 1.0 / t_cpu, "unit": "matvec/s", "cores": 1, "kind": "port",
+                                "sample": f"{n_cpu} full matvecs of the oracle port on the same "
+                                          "operator (oracle/packed_matvec.py, 1 BLAS thread)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    rep.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -46,22 +46,26 @@ class PlanStats(C.Structure):
 
 # every symbol include/h2g.h declares (checked by tests/test_abi.py)
 H2G_SYMBOLS = ("h2g_plan_create", "h2g_plan_destroy", "h2g_plan_get_stats", "h2g_matvec",
-               "h2g_matvec_host", "h2g_profile_phases", "h2g_launches_per_matvec",
+               "h2g_matvec_host", "h2g_profile_phases", "h2g_schedule_info",
+               "h2g_launches_per_matvec",
                "h2g_error_string", "h2g_last_error_detail", "h2g_abi_version")
 
 _LIB = None
 
 
 def lib_path() -> str:
-    return os.path.join(LIBDIR, "libh2g.so")
+    # H2G_LIB_PATH: load an alternative build (diagnostic builds in experiments)
+    return os.environ.get("H2G_LIB_PATH") or os.path.join(LIBDIR, "libh2g.so")
 
 
-def load() -> C.CDLL:
-    """Load libh2g.so (raises if it was not built)."""
+def load(path: str = None) -> C.CDLL:
+    """Load libh2g.so (raises if it was not built).  ``path`` loads a specific
+    build uncached (side-by-side variants in experiments)."""
     global _LIB
-    if _LIB is not None:
+    if path is None and _LIB is not None:
         return _LIB
-    path = lib_path()
+    explicit = path is not None
+    path = path or lib_path()
     if not os.path.exists(path):
         raise RuntimeError(
             f"native library {path} is missing; build it with "
@@ -76,19 +80,21 @@ def load() -> C.CDLL:
     L.h2g_profile_phases.argtypes = [vp, vp, vp, C.c_int, P_F64, P_I64,
                                      C.POINTER(C.c_char_p), C.c_int, C.POINTER(C.c_int)]
     L.h2g_launches_per_matvec.argtypes = [vp, C.c_int64]
+    L.h2g_schedule_info.argtypes = [C.POINTER(ExportDesc), C.c_int, C.c_char_p, C.c_int64]
     L.h2g_error_string.argtypes = [C.c_int]
     L.h2g_error_string.restype = C.c_char_p
     L.h2g_last_error_detail.restype = C.c_char_p
     if L.h2g_abi_version() != H2G_ABI_VERSION:
         raise RuntimeError("libh2g.so ABI version mismatch; rebuild it")
-    _LIB = L
+    if not explicit:
+        _LIB = L
     return L
 
 
-def check(rc: int, what: str = "h2g"):
+def check(rc: int, what: str = "h2g", L=None):
     if rc == H2G_OK:
         return
-    L = load()
+    L = L or load()
     msg = L.h2g_error_string(rc).decode()
     detail = L.h2g_last_error_detail().decode()
     if rc == H2G_ERR_LENGTH_MISMATCH:

@@ -75,6 +75,23 @@ struct HostSchedule {
 
 constexpr int kBlrChunkDoubles = 16384;  // split-K chunk of a BLR V^T q product
 
+struct HostChunk {      // streaming chunk before decoding into a ChunkRec
+  int64_t a_off;        // blob offset (doubles) of the first operator entry
+  int64_t y_off;        // arena slot of y[0] of the owning task
+  int32_t lda;          // == m: contiguous run (one copy); else per-column copies
+  int32_t m;
+  int32_t ncols;
+  int32_t flags;
+  int32_t seg_begin;    // segments [seg_begin, seg_begin + n_seg)
+  int32_t n_seg;
+};
+
+struct Seg {
+  int64_t x_off;        // arena slot of x for the segment's first column
+  int32_t ncols;
+  int32_t pad;
+};
+
 }  // namespace
 
 struct h2g_plan {
@@ -93,8 +110,7 @@ struct h2g_plan {
   ReduceJob* d_jobs = nullptr;
   std::vector<Phase> phases;
   int64_t n_tasks = 0, n_terms = 0;
-  Chunk* d_chunks = nullptr;
-  Seg* d_segs = nullptr;
+  ChunkRec* d_recs = nullptr;
   int64_t* d_cta = nullptr;
   int64_t n_chunks = 0;
   int engine = 1;  // 1 = TMA-bulk streaming engine, 0 = direct-load task kernel
@@ -396,7 +412,8 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
 // term starts where the previous ends, e.g. the M2L row of one target or the
 // near blocks of one leaf) share chunks, one x segment per term.
 void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
-                  std::vector<Chunk>& chunks, std::vector<Seg>& segs, std::vector<int64_t>& cta) {
+                  std::vector<HostChunk>& chunks, std::vector<Seg>& segs,
+                  std::vector<int64_t>& cta) {
   for (Phase& ph : phases) {
     if (ph.kind != PH_GEMV) continue;
     const int64_t nt = ph.task_end - ph.task_begin;
@@ -414,22 +431,29 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
         const Term& tm = s.terms[k];
         const bool strided = tm.lda != t.m;
         const int64_t ldas = strided ? ((t.m + 1) & ~1) + 2 : t.m;
-        const int64_t per = std::max<int64_t>(
+        int64_t per = std::max<int64_t>(
             1, std::min<int64_t>(kChunkCols, kChunkA / std::max<int64_t>(ldas, 1)));
+        if (strided) per = std::min<int64_t>(per, kMaxCopies);  // one bulk copy per column
         int64_t c0 = 0;
         while (c0 < tm.ncols) {
           const int64_t a_here = tm.a_off + c0 * tm.lda;
           int64_t take;
-          if (open && !strided && a_here == a_end && chunks.back().n_seg < kMaxSeg &&
-              chunks.back().ncols < per_open) {
+          const bool x_adjacent =
+              open && !segs.empty() && segs.back().x_off + segs.back().ncols == tm.x_off + c0;
+          if (open && !strided && a_here == a_end &&
+              (chunks.back().n_seg < kMaxSeg || x_adjacent) && chunks.back().ncols < per_open) {
             take = std::min<int64_t>(tm.ncols - c0, per_open - chunks.back().ncols);
-            Seg sg{tm.x_off + c0, (int32_t)take, 0};
-            segs.push_back(sg);
-            chunks.back().n_seg += 1;
+            if (x_adjacent) {  // x continues the previous segment: one copy serves both
+              segs.back().ncols += (int32_t)take;
+            } else {
+              Seg sg{tm.x_off + c0, (int32_t)take, 0};
+              segs.push_back(sg);
+              chunks.back().n_seg += 1;
+            }
             chunks.back().ncols += (int32_t)take;
           } else {
             take = std::min<int64_t>(tm.ncols - c0, per);
-            Chunk c;
+            HostChunk c;
             c.a_off = a_here;
             c.y_off = t.y_off;
             c.lda = tm.lda;
@@ -451,7 +475,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
         if (strided) open = false;
       }
       if ((int64_t)chunks.size() == task_chunk0[ti]) {  // no terms: writes zeros
-        Chunk c{};
+        HostChunk c{};
         c.y_off = t.y_off;
         c.lda = t.m;
         c.m = t.m;
@@ -486,6 +510,64 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
   }
 }
 
+// Decode every chunk into the 256-byte record the device producer executes:
+// alignment shifts, smem placement and the exact TMA bulk-copy list.  Needs
+// the device base addresses (blob and arena are 256-byte aligned).
+void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& segs,
+                  const double* d_blob, const double* d_arena, std::vector<ChunkRec>& recs) {
+  recs.resize(chunks.size());
+  const uint64_t blob = (uint64_t)(uintptr_t)d_blob, arena = (uint64_t)(uintptr_t)d_arena;
+  auto round16 = [](int64_t b) { return (uint32_t)((b + 15) & ~int64_t(15)); };
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    const HostChunk& c = chunks[i];
+    ChunkRec& r = recs[i];
+    memset(&r, 0, sizeof r);
+    r.y_off = c.y_off;
+    r.m = c.m;
+    r.ncols = c.ncols;
+    r.flags = c.flags;
+    r.n_seg = c.n_seg;
+    uint32_t total = 0;
+    int nc = 0;
+    if (c.ncols > 0) {
+      const bool strided = c.lda != c.m;
+      if (!strided) {
+        const int64_t sh = c.a_off & 1;
+        r.ldas = c.m;
+        r.a_shift = (int32_t)sh;
+        CopyDesc& d = r.copies[nc++];
+        d.src = blob + 8 * (uint64_t)(c.a_off - sh);
+        d.dst = 0;
+        d.bytes = round16(8 * (sh + (int64_t)c.m * c.ncols));
+        total += d.bytes;
+      } else {
+        r.ldas = ((c.m + 1) & ~1) + 2;
+        r.a_shift = (int32_t)(c.a_off & 1);
+        r.odd_lda = (c.lda & 1) ? 1 : 0;
+        for (int k = 0; k < c.ncols; ++k) {
+          const int64_t off = c.a_off + (int64_t)k * c.lda;
+          const int64_t sh = off & 1;
+          CopyDesc& d = r.copies[nc++];
+          d.src = blob + 8 * (uint64_t)(off - sh);
+          d.dst = (uint32_t)(8 * (int64_t)k * r.ldas);
+          d.bytes = round16(8 * (sh + c.m));
+          total += d.bytes;
+        }
+      }
+      int64_t col = 0;
+      for (int k = 0; k < c.n_seg; ++k) {
+        const Seg& sg = segs[c.seg_begin + k];
+        r.seg_c0[k] = (int16_t)col;
+        r.seg_src[k] = arena + 8 * (uint64_t)sg.x_off;
+        col += sg.ncols;
+      }
+      r.seg_c0[c.n_seg] = (int16_t)col;
+    }
+    r.n_copies = nc;
+    r.bytes_a = total;
+  }
+}
+
 inline int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 8));
@@ -496,7 +578,7 @@ int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s) {
   if (n <= 0) return H2G_OK;
   if (ph.kind == PH_GEMV && p->engine == 1) {
     stream_gemv_kernel<<<ph.n_cta, kStreamThreads, kStreamSmem, s>>>(
-        p->d_chunks, p->d_segs, p->d_cta + ph.cta_off, p->d_blob, p->d_arena);
+        p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
   } else if (ph.kind == PH_GEMV) {
     gemv_tasks_kernel<<<(unsigned)n, kWarps * 32, 0, s>>>(p->d_tasks + ph.task_begin, p->d_terms,
                                                           p->d_blob, p->d_arena);
@@ -538,8 +620,7 @@ void free_plan(h2g_plan* p) {
   cudaFree(p->d_tasks);
   cudaFree(p->d_terms);
   cudaFree(p->d_jobs);
-  cudaFree(p->d_chunks);
-  cudaFree(p->d_segs);
+  cudaFree(p->d_recs);
   cudaFree(p->d_cta);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
@@ -576,10 +657,10 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
         nsm > 0)
       p->n_sm = nsm;
   }
-  std::vector<Chunk> chunks;
+  std::vector<HostChunk> chunks;
   std::vector<int64_t> cta;
   std::vector<Seg> segs;
-  build_chunks(s, s.phases, p->n_sm, chunks, segs, cta);
+  build_chunks(s, s.phases, p->n_sm * kCtasPerSm, chunks, segs, cta);
   p->n_chunks = (int64_t)chunks.size();
   p->phases = s.phases;
   p->n_tasks = (int64_t)s.tasks.size();
@@ -611,18 +692,20 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
     if ((r = upload((void**)&p->d_tasks, s.tasks.data(), sizeof(Task) * s.tasks.size()))) return r;
     if ((r = upload((void**)&p->d_terms, s.terms.data(), sizeof(Term) * s.terms.size()))) return r;
     if ((r = upload((void**)&p->d_jobs, s.jobs.data(), sizeof(ReduceJob) * s.jobs.size()))) return r;
-    if ((r = upload((void**)&p->d_chunks, chunks.data(), sizeof(Chunk) * chunks.size()))) return r;
     if ((r = upload((void**)&p->d_cta, cta.data(), sizeof(int64_t) * cta.size()))) return r;
-    if ((r = upload((void**)&p->d_segs, segs.data(), sizeof(Seg) * segs.size()))) return r;
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kStreamSmem));
     // +8 slots of slack: aligned bulk copies of x may read up to 8 bytes past a slice
     CUDA_TRY(cudaMalloc((void**)&p->d_arena, sizeof(double) * (p->n_slots + 8)));
     CUDA_TRY(cudaMemset(p->d_arena, 0, sizeof(double) * (p->n_slots + 8)));
+    {
+      std::vector<ChunkRec> recs;
+      make_records(chunks, segs, p->d_blob, p->d_arena, recs);
+      if ((r = upload((void**)&p->d_recs, recs.data(), sizeof(ChunkRec) * recs.size()))) return r;
+    }
     p->workspace_bytes = sizeof(double) * p->n_slots + sizeof(Task) * s.tasks.size() +
                          sizeof(Term) * s.terms.size() + sizeof(ReduceJob) * s.jobs.size() +
-                         sizeof(Chunk) * chunks.size() + sizeof(int64_t) * cta.size() +
-                         sizeof(Seg) * segs.size() +
+                         sizeof(ChunkRec) * chunks.size() + sizeof(int64_t) * cta.size() +
                          sizeof(int32_t) * p->N;
     // capture the fixed middle phases into one CUDA graph
     CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
@@ -746,6 +829,50 @@ int h2g_matvec_host(h2g_plan* p, const double* q_host, double* phi_host, int64_t
   cudaFreeAsync(dphi, p->stream);
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   return rc;
+}
+
+int h2g_schedule_info(const h2g_export_desc* desc, int n_sm, char* buf, int64_t buflen) {
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!buf || buflen <= 0 || n_sm <= 0) return fail(H2G_ERR_INVALID_ARG, "bad buffer / n_sm");
+  h2g_plan tmp;
+  HostSchedule s;
+  rc = build_schedule(desc, &tmp, s);
+  if (rc) return rc;
+  std::vector<HostChunk> chunks;
+  std::vector<int64_t> cta;
+  std::vector<Seg> segs;
+  build_chunks(s, s.phases, n_sm * kCtasPerSm, chunks, segs, cta);
+  std::string out = "{\"n_slots\": " + std::to_string(tmp.n_slots) + ", \"phases\": [";
+  for (size_t i = 0; i < s.phases.size(); ++i) {
+    const Phase& ph = s.phases[i];
+    int64_t nch = 0, bytes = 0, maxcta = 0, nseg = 0;
+    if (ph.kind == PH_GEMV) {
+      for (int32_t g = 0; g < ph.n_cta; ++g) {
+        int64_t cb = 0;
+        for (int64_t c = cta[ph.cta_off + g]; c < cta[ph.cta_off + g + 1]; ++c) {
+          cb += 8LL * chunks[c].m * chunks[c].ncols;
+          nseg += chunks[c].n_seg;
+          ++nch;
+        }
+        bytes += cb;
+        maxcta = std::max(maxcta, cb);
+      }
+    }
+    char line[512];
+    snprintf(line, sizeof line,
+             "%s{\"name\": \"%s\", \"kind\": %d, \"tasks\": %lld, \"chunks\": %lld, "
+             "\"segs\": %lld, \"ctas\": %d, \"a_bytes\": %lld, \"max_cta_bytes\": %lld, "
+             "\"alg_bytes\": %lld}",
+             i ? ", " : "", ph.name.c_str(), ph.kind, (long long)(ph.task_end - ph.task_begin),
+             (long long)nch, (long long)nseg, ph.n_cta, (long long)bytes, (long long)maxcta,
+             (long long)ph.alg_bytes);
+    out += line;
+  }
+  out += "]}";
+  if ((int64_t)out.size() + 1 > buflen) return fail(H2G_ERR_INVALID_ARG, "buffer too small");
+  memcpy(buf, out.c_str(), out.size() + 1);
+  return H2G_OK;
 }
 
 int h2g_profile_phases(h2g_plan* p, const double* q_dev, double* phi_dev, int iters, double* ms,

@@ -2,26 +2,31 @@
 //
 // The matvec is HBM-bound: every stored operator scalar is used in exactly
 // one multiply-add (0.25 flop/B).  The engine keeps many
-// bytes in flight per SM without spending registers on them:
+// bytes in flight per SM without spending registers or issue slots on them:
 //
 //   * the host cuts every task (one output slice y[0:m), see h2g_kernels.cuh)
-//     into CHUNKS of <= kChunkA doubles of operator data: a run of whole
-//     columns that is contiguous in the blob (possibly spanning several terms
-//     of the task, e.g. all M2L blocks of one target) plus, per term, the
-//     matching slice of the input vector x (a "segment");
-//   * one persistent CTA per SM owns a contiguous range of chunks (whole
-//     tasks, balanced by bytes on the host);
-//   * warp 0 is the producer: its lanes fetch 32 chunk headers at a time
-//     (coalesced, prefetched one batch ahead), then one elected lane waits for
-//     a free ring stage, writes the chunk's decoded header into shared memory
-//     and issues cp.async.bulk copies (TMA bulk, SASS UBLKCP) of the operator
-//     columns and of every x segment, completing on the stage's mbarrier
-//     (arrive.expect_tx);
-//   * warps 1..kConsumers are consumers: they wait on the stage's mbarrier,
-//     read the column-major chunk from shared memory (lane = row,
-//     conflict-free), accumulate in registers, release the stage, and at the
-//     end of a task reduce the warps' partial sums in a fixed order and store
-//     y once.
+//     into CHUNKS of <= kChunkA doubles of operator data -- a run of whole
+//     columns contiguous in the blob (possibly spanning several terms of the
+//     task, e.g. the whole M2L row of a target) -- plus, per term, the slice of
+//     the input vector x it multiplies (a "segment"; adjacent slices merge);
+//   * every chunk is pre-decoded on the host into a 256-byte RECORD: the
+//     consumer header (rows, columns, smem stride, alignment shift, segment
+//     table) and the exact list of TMA bulk copies (absolute global source,
+//     smem destination, bytes) that stage its operator data;
+//   * one persistent CTA per SM-slot owns a contiguous range of records (whole
+//     tasks, balanced by bytes on the host); kCtasPerSm pipelines per SM;
+//   * warp 0 is the producer: lane 0 bulk-copies records kRecAhead chunks
+//     ahead into a record ring (own mbarriers); for chunk i it waits for a free
+//     data stage, arms the stage mbarrier (arrive.expect_tx) and lane k issues
+//     the record's k-th cp.async.bulk (SASS UBLKCP);
+//   * warps 1..kConsumers consume.  Warp cw owns chunk columns
+//     c = cw + kConsumers*t.  One chunk ahead it loads the x values of its
+//     columns from L2 into registers (latency hidden behind the current
+//     chunk), parks them in a per-warp smem strip, waits for the stage, and
+//     runs a regular loop: LDS.128 broadcast of two x values, one LDS.64 of A
+//     per 32 rows per column, DFMA into per-lane row accumulators (no
+//     cross-lane reduction).  It releases the stage, and at a task's last chunk
+//     the warps' partial sums are reduced in fixed order and y stored once.
 //
 // Determinism: a task lives in one CTA; each warp accumulates its columns in
 // a fixed order; warps are combined in warp order.  No atomics.
@@ -30,53 +35,64 @@
 
 namespace h2g {
 
-struct Chunk {          // 40 bytes, host-built
-  int64_t a_off;        // blob offset (doubles) of the first operator entry
+// Tunables (macro overrides exist for diagnostic builds only).
+#ifndef H2G_CONSUMERS
+#define H2G_CONSUMERS 4
+#endif
+#ifndef H2G_CTAS_PER_SM
+#define H2G_CTAS_PER_SM 2
+#endif
+#ifndef H2G_STAGES
+#define H2G_STAGES 3
+#endif
+#ifndef H2G_CHUNK_A
+#define H2G_CHUNK_A 4096
+#endif
+constexpr int kLastOfTask = 1;
+constexpr int kConsumers = H2G_CONSUMERS;     // consumer warps per CTA
+constexpr int kStreamThreads = 32 * (1 + kConsumers);
+constexpr int kCtasPerSm = H2G_CTAS_PER_SM;   // independent pipelines per SM
+constexpr int kStages = H2G_STAGES;           // data ring depth (per CTA)
+constexpr int kRecRing = 16;                  // record ring depth
+constexpr int kRecAhead = 8;                  // records prefetched ahead of the producer
+constexpr int kChunkA = H2G_CHUNK_A;          // doubles of operator data per chunk (32 KB)
+constexpr int kChunkCols = 64 * kConsumers;   // max columns per chunk (64 per warp)
+constexpr int kMaxCopies = 6;                 // operator bulk copies per chunk (record capacity)
+constexpr int kMaxSeg = 9;                    // x segments per chunk
+constexpr int kStageA = kChunkA + 8;          // + alignment slack
+constexpr int kStreamMaxRows = 256;
+constexpr int kXStrip = 64 + 4;               // per-warp x strip (doubles)
+static_assert(kRecRing >= kStages + kRecAhead, "record ring too shallow");
+
+struct CopyDesc {       // 16 bytes
+  uint64_t src;         // absolute global address (16-byte aligned)
+  uint32_t dst;         // byte offset inside the data stage (16-byte aligned)
+  uint32_t bytes;       // multiple of 16
+};
+
+struct ChunkRec {       // 256 bytes, host-built, TMA-copied into the record ring
   int64_t y_off;        // arena slot of y[0] of the owning task
-  int32_t lda;          // == m: contiguous run (one copy); else per-column copies
   int32_t m;            // rows of the task (<= kStreamMaxRows)
   int32_t ncols;        // columns in this chunk
   int32_t flags;        // kLastOfTask
-  int32_t seg_begin;    // x segments [seg_begin, seg_begin + n_seg) in Seg[]
-  int32_t n_seg;
+  int32_t n_seg;        // x segments
+  int32_t ldas;         // column stride of A in smem (doubles)
+  int32_t a_shift;      // A(0, 0) at sA + a_shift (odd_lda: shift of column 0)
+  int32_t odd_lda;      // per-column copies whose alignment shift alternates
+  int32_t n_copies;     // operator bulk copies
+  uint32_t bytes_a;     // sum of operator copy bytes (expect_tx)
+  int32_t pad0;
+  int16_t seg_c0[kMaxSeg + 1];  // first chunk column of segment k (+ end sentinel)
+  int16_t pad1[kMaxSeg + 1];
+  uint64_t seg_src[kMaxSeg];    // absolute address of x for segment k's first column
+  CopyDesc copies[kMaxCopies];
 };
+static_assert(sizeof(ChunkRec) == 256, "record layout");
 
-struct Seg {            // 16 bytes: x slice of consecutive chunk columns
-  int64_t x_off;        // arena slot of x for the segment's first column
-  int32_t ncols;
-  int32_t pad;
-};
-
-constexpr int kLastOfTask = 1;
-constexpr int kConsumers = 4;                 // consumer warps per CTA
-constexpr int kStreamThreads = 32 * (1 + kConsumers);
-constexpr int kStages = 8;                    // ring depth
-constexpr int kChunkA = 2048;                 // doubles of operator data per chunk (16 KB)
-constexpr int kChunkCols = 256;               // max columns per chunk
-constexpr int kMaxSeg = 16;                   // max x segments per chunk
-constexpr int kStageX = kChunkCols + 2 * kMaxSeg + 4;  // x slots incl. alignment slack
-constexpr int kStageA = kChunkA + 8;
-constexpr int kStageDoubles = kStageA + kStageX;
-constexpr int kStreamMaxRows = 256;
-
-struct StageHdr {       // decoded by the producer, read by consumers (smem)
-  int64_t y_off;
-  int32_t m, ncols, flags, n_seg;
-  int32_t ldas;         // column stride in smem
-  int32_t a_shift;      // first operator entry at sA + a_shift (contiguous runs)
-  int32_t strided;      // 1: per-column copies, column c at sA + c*ldas + shift_c
-  int32_t odd_lda;      // strided with odd lda: per-column shift alternates
-  int32_t a_shift0;     // shift of column 0 (strided)
-  int32_t pad;
-  int16_t seg_c0[kMaxSeg];   // first chunk column of segment k
-  int16_t seg_x[kMaxSeg];    // smem x index of segment k's first value
-};
-
-constexpr size_t kHdrBytes = ((sizeof(StageHdr) + 15) / 16) * 16;
-constexpr size_t kStreamSmem = (size_t)kStages * kStageDoubles * 8 +
+constexpr size_t kStreamSmem = (size_t)kStages * kStageA * 8 +
                                (size_t)kConsumers * kStreamMaxRows * 8 +
-                               (size_t)kStages * kHdrBytes + 2 * kStages * 8 +
-                               (size_t)32 * kMaxSeg * sizeof(Seg);
+                               (size_t)kConsumers * kXStrip * 8 + (size_t)kRecRing * 256 +
+                               (size_t)(2 * kStages + kRecRing) * 8;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -120,243 +136,199 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-__device__ __forceinline__ int dshift(const double* p) {
-  return (int)((((uintptr_t)p) & 15) >> 3);
-}
-
-// bytes of an aligned-down copy of n doubles starting at p
-__device__ __forceinline__ uint32_t span_bytes(const double* p, int n) {
-  return (uint32_t)(((dshift(p) + n) * 8 + 15) & ~15);
-}
-
-__device__ __forceinline__ const double* align_down(const double* p) {
-  return (const double*)(((uintptr_t)p) & ~(uintptr_t)15);
-}
-
-__device__ __forceinline__ Chunk shfl_chunk(const Chunk& c, int src) {
-  Chunk o;
-  o.a_off = __shfl_sync(0xffffffffu, c.a_off, src);
-  o.y_off = __shfl_sync(0xffffffffu, c.y_off, src);
-  o.lda = __shfl_sync(0xffffffffu, c.lda, src);
-  o.m = __shfl_sync(0xffffffffu, c.m, src);
-  o.ncols = __shfl_sync(0xffffffffu, c.ncols, src);
-  o.flags = __shfl_sync(0xffffffffu, c.flags, src);
-  o.seg_begin = __shfl_sync(0xffffffffu, c.seg_begin, src);
-  o.n_seg = __shfl_sync(0xffffffffu, c.n_seg, src);
-  return o;
-}
-
 // ---------------------------------------------------------------- consumer
-// columns [c_begin, c_end) of a chunk whose column c is at As + c*ldas and
-// whose x value is xs[c - c_begin]; warp cw takes c_begin+cw, +kConsumers, ...
-template <int J>
-__device__ __forceinline__ void consume_cols(const double* __restrict__ As, int ldas,
-                                             const double* __restrict__ xs, int c_begin,
-                                             int c_end, int m, int lane, int cw, double* acc) {
-  double r0[J], r1[J];
+// x of the warp's local columns t = lane and t = lane + 32 (chunk column
+// c = cw + kConsumers * t), loaded from global (L2); 0 past the chunk.
+__device__ __forceinline__ void fetch_x(const ChunkRec& h, int lane, int cw, double* xr) {
+  const int ncols = h.ncols, n_seg = h.n_seg;
+  int c0[kMaxSeg];
 #pragma unroll
-  for (int j = 0; j < J; ++j) r0[j] = r1[j] = 0.0;
-  int c = c_begin + cw;
-  for (; c + kConsumers < c_end; c += 2 * kConsumers) {
-    const double x0 = xs[c - c_begin];
-    const double x1 = xs[c + kConsumers - c_begin];
-    const double* col0 = As + c * ldas;
-    const double* col1 = col0 + kConsumers * ldas;
+  for (int k = 0; k < kMaxSeg; ++k) c0[k] = h.seg_c0[k];
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int rr = lane + 32 * j;
-      if (rr < m) {
-        r0[j] = fma(col0[rr], x0, r0[j]);
-        r1[j] = fma(col1[rr], x1, r1[j]);
+  for (int q = 0; q < 2; ++q) {
+    const int c = cw + kConsumers * (lane + 32 * q);
+    int k = 0, start = c0[0];
+#pragma unroll
+    for (int j = 1; j < kMaxSeg; ++j)
+      if (j < n_seg && c >= c0[j]) {  // segments are ascending: the last hit wins
+        k = j;
+        start = c0[j];
       }
-    }
+    xr[q] = c < ncols ? __ldg(reinterpret_cast<const double*>(h.seg_src[k]) + (c - start)) : 0.0;
   }
-  if (c < c_end) {
-    const double x0 = xs[c - c_begin];
-    const double* col0 = As + c * ldas;
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int rr = lane + 32 * j;
-      if (rr < m) r0[j] = fma(col0[rr], x0, r0[j]);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < J; ++j) acc[j] += r0[j] + r1[j];
 }
 
+// One chunk: warp cw owns columns c = cw + kConsumers * t, t < T.  xs holds the
+// x values of those columns (xs[t]); column t at As + t * kConsumers * ldas.
+// Rows >= m are computed from whatever lies in shared memory and discarded.
 template <int J>
-__device__ __forceinline__ void consume_stage(const StageHdr& h, const double* sA,
-                                              const double* sX, int lane, int cw, double* acc) {
-  const double* As = sA + h.a_shift;
-  for (int k = 0; k < h.n_seg; ++k) {
-    const int c0 = h.seg_c0[k];
-    const int c1 = (k + 1 < h.n_seg) ? h.seg_c0[k + 1] : h.ncols;
-    consume_cols<J>(As, h.ldas, sX + h.seg_x[k], c0, c1, h.m, lane, cw, acc);
+__device__ __forceinline__ void consume_stage(const double* __restrict__ As, int ldas, int T,
+                                              const double* __restrict__ xs, int lane,
+                                              double* acc) {
+  constexpr int U = J == 1 ? 8 : (J == 2 ? 4 : 2);  // columns in flight per iteration
+  double r[U][J];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int j = 0; j < J; ++j) r[u][j] = 0.0;
+  const double* base = As + lane;
+  const int step = kConsumers * ldas;
+  int t = 0;
+  for (; t + U <= T; t += U) {
+    double xv[U], a[U][J];
+#pragma unroll
+    for (int u = 0; u < U; u += 2) {
+      const double2 x2 = *reinterpret_cast<const double2*>(xs + t + u);
+      xv[u] = x2.x;
+      xv[u + 1] = x2.y;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double* col = base + (t + u) * step;
+#pragma unroll
+      for (int j = 0; j < J; ++j) a[u][j] = col[32 * j];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < J; ++j) r[u][j] = fma(a[u][j], xv[u], r[u][j]);
+  }
+  for (; t < T; ++t) {
+    const double x0 = xs[t];
+    const double* col = base + t * step;
+#pragma unroll
+    for (int j = 0; j < J; ++j) r[0][j] = fma(col[32 * j], x0, r[0][j]);
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    double tsum = r[0][j];
+#pragma unroll
+    for (int u = 1; u < U; ++u) tsum += r[u][j];
+    acc[j] += tsum;
   }
 }
 
-__global__ void __launch_bounds__(kStreamThreads, 1)
-stream_gemv_kernel(const Chunk* __restrict__ chunks, const Seg* __restrict__ segs,
-                   const int64_t* __restrict__ cta_begin, const double* __restrict__ blob,
+__global__ void __launch_bounds__(kStreamThreads, kCtasPerSm)
+stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__ cta_begin,
                    double* arena) {
   extern __shared__ __align__(128) double smem[];
   double* stage_buf = smem;
-  double* red = smem + (size_t)kStages * kStageDoubles;
-  StageHdr* hdr = reinterpret_cast<StageHdr*>(red + kConsumers * kStreamMaxRows);
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(hdr) + kStages * kHdrBytes);
+  double* red = smem + (size_t)kStages * kStageA;
+  double* xstrip = red + kConsumers * kStreamMaxRows;
+  ChunkRec* rring = reinterpret_cast<ChunkRec*>(xstrip + kConsumers * kXStrip);
+  uint64_t* full = reinterpret_cast<uint64_t*>(rring + kRecRing);
   uint64_t* empty = full + kStages;
-  Seg* seg_scratch = reinterpret_cast<Seg*>(empty + kStages);
+  uint64_t* recbar = empty + kStages;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t cb = cta_begin[blockIdx.x];
-  const int64_t ce = cta_begin[blockIdx.x + 1];
+  const int n = (int)(cta_begin[blockIdx.x + 1] - cb);
+  const ChunkRec* my = recs + cb;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers);
     }
+    for (int r = 0; r < kRecRing; ++r) mbar_init(&recbar[r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   if (warp == 0) {
     // ------------------------------------------------ producer warp
-    Chunk cur{}, nxt{};
-    if (cb + lane < ce) cur = chunks[cb + lane];
-    if (cb + 32 + lane < ce) nxt = chunks[cb + 32 + lane];
-    for (int64_t base = cb; base < ce; base += 32) {
-      const int nb = (int)(ce - base < 32 ? ce - base : 32);
-      // stage this batch's segment descriptors (consecutive in segs[]) in smem
-      const int seg_base = __shfl_sync(0xffffffffu, cur.seg_begin, 0);
-      const int seg_end = __shfl_sync(0xffffffffu, cur.seg_begin + cur.n_seg, nb - 1);
-      for (int e = lane; e < seg_end - seg_base; e += 32) seg_scratch[e] = segs[seg_base + e];
-      __syncwarp();
-      for (int k = 0; k < nb; ++k) {
-        const Chunk ch = shfl_chunk(cur, k);
-        // lanes < n_seg take the segment descriptors of this chunk (smem copy)
-        Seg sg{};
-        if (lane < ch.n_seg) sg = seg_scratch[ch.seg_begin - seg_base + lane];
-        const int it = (int)(base + k - cb);
-        const int s = it % kStages;
-        const uint32_t ph = (uint32_t)(it / kStages) & 1u;
-        // per-segment x placement (prefix over lanes)
-        const double* xsrc = arena + sg.x_off;
-        const uint32_t xb = lane < ch.n_seg ? span_bytes(xsrc, sg.ncols) : 0u;
-        uint32_t xpos = xb;  // inclusive scan of bytes
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t v = __shfl_up_sync(0xffffffffu, xpos, o);
-          if (lane >= o) xpos += v;
-        }
-        const uint32_t x_total = __shfl_sync(0xffffffffu, xpos, 31);
-        xpos -= xb;  // exclusive
-        int ccol = sg.ncols;  // column prefix
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, ccol, o);
-          if (lane >= o) ccol += v;
-        }
-        ccol -= sg.ncols;
-        double* sA = stage_buf + (size_t)s * kStageDoubles;
-        double* sX = sA + kStageA;
-        StageHdr* h = reinterpret_cast<StageHdr*>(reinterpret_cast<char*>(hdr) + s * kHdrBytes);
-        if (lane == 0) mbar_wait(&empty[s], ph ^ 1u);
-        __syncwarp();
-        if (lane < ch.n_seg) {
-          h->seg_c0[lane] = (int16_t)ccol;
-          h->seg_x[lane] = (int16_t)(xpos / 8 + dshift(xsrc));
-        }
-        __syncwarp();  // segment table before lane 0's release (arrive) below
-        const bool strided = ch.lda != ch.m;
-        const double* a0 = blob + ch.a_off;
-        uint32_t a_total = 0;
-        if (!strided) {
-          a_total = ch.ncols > 0 ? span_bytes(a0, ch.m * ch.ncols) : 0u;
-        } else {
-          for (int c = lane; c < ch.ncols; c += 32)
-            a_total += span_bytes(a0 + (int64_t)c * ch.lda, ch.m);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) a_total += __shfl_xor_sync(0xffffffffu, a_total, o);
-        }
-        const int ldas = strided ? ((ch.m + 1) & ~1) + 2 : ch.m;
-        if (lane == 0) {
-          h->y_off = ch.y_off;
-          h->m = ch.m;
-          h->ncols = ch.ncols;
-          h->flags = ch.flags;
-          h->n_seg = ch.n_seg;
-          h->ldas = ldas;
-          h->strided = strided;
-          h->odd_lda = strided && (ch.lda & 1);
-          h->a_shift = dshift(a0);
-          h->a_shift0 = dshift(a0);
-          mbar_arrive_expect_tx(&full[s], a_total + x_total);
-        }
-        __syncwarp();
-        // issue the copies: x segments by their lanes, operator data by lane 0
-        // (contiguous) or by column-strided lanes (strided)
-        if (lane < ch.n_seg && sg.ncols > 0)
-          bulk_g2s(reinterpret_cast<char*>(sX) + xpos, align_down(xsrc), xb, &full[s]);
-        if (!strided) {
-          if (lane == 0 && a_total) bulk_g2s(sA, align_down(a0), a_total, &full[s]);
-        } else {
-          for (int c = lane; c < ch.ncols; c += 32) {
-            const double* src = a0 + (int64_t)c * ch.lda;
-            bulk_g2s(sA + (size_t)c * ldas, align_down(src), span_bytes(src, ch.m), &full[s]);
-          }
-        }
-        __syncwarp();
+    if (lane == 0)
+      for (int j = 0; j < kRecAhead && j < n; ++j) {
+        mbar_arrive_expect_tx(&recbar[j], sizeof(ChunkRec));
+        bulk_g2s(&rring[j], my + j, sizeof(ChunkRec), &recbar[j]);
       }
-      cur = nxt;
-      if (base + 64 + lane < ce) nxt = chunks[base + 64 + lane];
+    for (int i = 0; i < n; ++i) {
+      const int s = i % kStages;
+      const int r = i % kRecRing;
+      if (lane == 0) {
+        mbar_wait(&empty[s], ((uint32_t)(i / kStages) & 1u) ^ 1u);
+        // consumers are done with chunk i - kStages; record slot (i + kRecAhead)
+        // % kRecRing last held chunk i + kRecAhead - kRecRing <= i - kStages
+        const int j = i + kRecAhead;
+        if (j < n) {
+          const int rj = j % kRecRing;
+          mbar_arrive_expect_tx(&recbar[rj], sizeof(ChunkRec));
+          bulk_g2s(&rring[rj], my + j, sizeof(ChunkRec), &recbar[rj]);
+        }
+      }
+      mbar_wait(&recbar[r], (uint32_t)(i / kRecRing) & 1u);
+      const ChunkRec& h = rring[r];
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], h.bytes_a);
+      __syncwarp();
+      if (lane < h.n_copies) {  // lane k issues operator copy k (TMA bulk)
+        const CopyDesc cd = h.copies[lane];
+        char* st = reinterpret_cast<char*>(stage_buf + (size_t)s * kStageA);
+        bulk_g2s(st + cd.dst, reinterpret_cast<const void*>(cd.src), cd.bytes, &full[s]);
+      }
+      __syncwarp();
     }
     return;
   }
 
   // ---------------------------------------------------- consumers
   const int cw = warp - 1;
+  double* xs = xstrip + cw * kXStrip;
   double acc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-  for (int64_t i = cb; i < ce; ++i) {
-    const int it = (int)(i - cb);
-    const int s = it % kStages;
-    const uint32_t ph = (uint32_t)(it / kStages) & 1u;
-    mbar_wait(&full[s], ph);
-    const StageHdr& h = *reinterpret_cast<const StageHdr*>(reinterpret_cast<const char*>(hdr) +
-                                                           s * kHdrBytes);
-    const double* sA = stage_buf + (size_t)s * kStageDoubles;
-    const double* sX = sA + kStageA;
+  double xn[2] = {0.0, 0.0};
+  if (n > 0) {
+    mbar_wait(&recbar[0], 0u);
+    fetch_x(rring[0], lane, cw, xn);
+  }
+  for (int i = 0; i < n; ++i) {
+    const int s = i % kStages;
+    const ChunkRec& h = rring[i % kRecRing];
     const int m = h.m;
-    if (h.ncols > 0) {
-      if (!h.odd_lda) {
-        const int J = (m + 31) >> 5;
-        switch (J) {
-          case 1: consume_stage<1>(h, sA, sX, lane, cw, acc); break;
-          case 2: consume_stage<2>(h, sA, sX, lane, cw, acc); break;
-          case 3: consume_stage<3>(h, sA, sX, lane, cw, acc); break;
-          case 4: consume_stage<4>(h, sA, sX, lane, cw, acc); break;
-          default: consume_stage<8>(h, sA, sX, lane, cw, acc); break;
-        }
-      } else {
-        // strided run with odd lda (rare): the alignment shift alternates per column
-        const double* xs = sX + h.seg_x[0];
-        for (int c = cw; c < h.ncols; c += kConsumers) {
-          const int sh = (h.a_shift0 + c) & 1;
-          const double* col = sA + (size_t)c * h.ldas + sh;
-          const double xv = xs[c];
+    const int ncols = h.ncols;
+    const int flags = h.flags;
+    const int ldas = h.ldas;
+    const int a_shift = h.a_shift;
+    const int odd = h.odd_lda;
+    const int64_t y_off = h.y_off;
+    // park this chunk's x, then issue the next chunk's x loads (used next iteration)
+    xs[lane] = xn[0];
+    xs[lane + 32] = xn[1];
+    if (i + 1 < n) {
+      mbar_wait(&recbar[(i + 1) % kRecRing], (uint32_t)((i + 1) / kRecRing) & 1u);
+      fetch_x(rring[(i + 1) % kRecRing], lane, cw, xn);
+    }
+    __syncwarp();
+    mbar_wait(&full[s], (uint32_t)(i / kStages) & 1u);
+    const double* sA = stage_buf + (size_t)s * kStageA;
+    const int T = ncols > cw ? (ncols - cw + kConsumers - 1) / kConsumers : 0;
+#ifndef H2G_DIAG_NOCOMPUTE
+    if (!odd) {
+      const double* As = sA + a_shift + cw * ldas;
+      const int J = (m + 31) >> 5;
+      if (J == 1)
+        consume_stage<1>(As, ldas, T, xs, lane, acc);
+      else if (J == 2)
+        consume_stage<2>(As, ldas, T, xs, lane, acc);
+      else if (J <= 4)
+        consume_stage<4>(As, ldas, T, xs, lane, acc);
+      else
+        consume_stage<8>(As, ldas, T, xs, lane, acc);
+    } else {
+      // per-column copies with odd lda (rare): alignment shift alternates
+      for (int t = 0; t < T; ++t) {
+        const int c = cw + kConsumers * t;
+        const double* col = sA + (size_t)c * ldas + ((a_shift + c) & 1);
+        const double xv = xs[t];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int rr = lane + 32 * j;
-            if (rr < m) acc[j] = fma(col[rr], xv, acc[j]);
-          }
+        for (int j = 0; j < 8; ++j) {
+          const int rr = lane + 32 * j;
+          if (rr < m) acc[j] = fma(col[rr], xv, acc[j]);
         }
       }
     }
-    const int flags = h.flags;
-    const int64_t y_off = h.y_off;
+#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (flags & kLastOfTask) {

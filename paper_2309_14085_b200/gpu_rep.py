@@ -94,8 +94,8 @@ def _torch():
 class GpuHierRep:
     """The operator of one reference ``HierRep``, resident on a B200."""
 
-    def __init__(self, op: PackedOperator, device: int = 0):
-        L = _lib.load()
+    def __init__(self, op: PackedOperator, device: int = 0, lib=None):
+        L = lib or _lib.load()
         op.validate()
         desc, keep = _desc_from_packed(op)
         plan = C.c_void_p()
@@ -234,6 +234,17 @@ class GpuHierRep:
                                               names, cap, C.byref(n)), "h2g_profile_phases")
         return [{"phase": names[i].decode(), "ms": ms[i], "bytes": int(by[i])}
                 for i in range(n.value)]
+
+
+def schedule_info(op: PackedOperator, n_sm: int = 148) -> dict:
+    """Host-only view of the device schedule (phases, chunks, CTA balance)."""
+    import json
+    L = _lib.load()
+    desc, keep = _desc_from_packed(op)
+    buf = C.create_string_buffer(1 << 20)
+    _lib.check(L.h2g_schedule_info(C.byref(desc), int(n_sm), buf, len(buf)), "h2g_schedule_info")
+    del keep
+    return json.loads(buf.value.decode())
 
 
 def torch_complex(re, im):
