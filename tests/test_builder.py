@@ -1,0 +1,101 @@
+"""Native builder (libh2b.so) against the reference construction.
+
+The golden fixtures hold the operators the reference's build_variant
+(engine.py:325-373) produced.  The native restatement must reproduce the
+tree (tree.py:111-185), the weak partition lists (partition.py:77-137), every
+NCA rank (engine.py:54-114 via lowrank.py:77-147), the BLR ranks
+(blr.py:46-69), the near lists and the mem_scalars tally, and its operator
+must act like the reference's: matvec equal to the reference's own output to
+roundoff, and the same error against the dense product.
+"""
+
+import numpy as np
+import pytest
+
+from golden_io import golden_names, load_golden, rel_err
+from oracle.packed_matvec import packed_matvec
+from paper_2309_14085_b200.builder import build_variant, jittered_grid, uniform_points
+
+NAMES = golden_names()
+
+
+def _native_for(name):
+    op, z, meta = load_golden(name)
+    pts = np.empty_like(op.points_tree)
+    pts[op.perm] = op.points_tree
+    nop = build_variant(meta["variant"], pts, kernel=meta["kernel"], n_max=meta["n_max"],
+                        eps=meta["eps"])
+    return op, nop, z, meta
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_structure_and_ranks_match_reference(name):
+    op, nop, z, meta = _native_for(name)
+    assert nop.kappa == op.kappa
+    assert np.array_equal(nop.perm, op.perm)
+    assert np.array_equal(nop.level_offset, op.level_offset)
+    assert np.array_equal(nop.cl_start, op.cl_start) and np.array_equal(nop.cl_end, op.cl_end)
+    assert len(nop.channels) == len(op.channels)
+    for a, b in zip(nop.channels, op.channels):
+        assert np.array_equal(a.r_in, b.r_in) and np.array_equal(a.r_out, b.r_out)
+        assert np.array_equal(a.m2l_rowptr, b.m2l_rowptr) and np.array_equal(a.m2l_src, b.m2l_src)
+        assert np.array_equal(a.p2m_off >= 0, b.p2m_off >= 0)
+        assert np.array_equal(a.m2m_off >= 0, b.m2m_off >= 0)
+        assert np.array_equal(a.l2l_off >= 0, b.l2l_off >= 0)
+    assert np.array_equal(nop.blr_rowptr, op.blr_rowptr)
+    assert np.array_equal(nop.blr_src, op.blr_src) and np.array_equal(nop.blr_rank, op.blr_rank)
+    assert np.array_equal(nop.near_rowptr, op.near_rowptr)
+    assert np.array_equal(nop.near_src, op.near_src)
+    assert nop.mem_scalars == op.mem_scalars == meta["mem_scalars"]
+    assert nop.stored_scalars() == nop.mem_scalars
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_native_operator_acts_like_reference(name):
+    op, nop, z, meta = _native_for(name)
+    phi = packed_matvec(nop, z["q"])
+    # identical pivots: only LU/BLAS roundoff (amplified by cross-matrix
+    # conditioning ~ 1/eps) separates the two operators
+    assert rel_err(phi, z["phi_ref"]) <= 1e-12
+    re = rel_err(phi, z["phi_dense"])
+    assert abs(re - meta["re_ref"]) <= 1e-3 * meta["re_ref"] + 1e-14
+
+
+def test_near_blocks_bitwise_equal_reference():
+    """Kernel entries are restated exactly (kernels.py:36-57): near blocks of
+    the native build equal the reference's to the last bit for 1/r."""
+    op, nop, z, meta = _native_for("g3d_lap_h2star")
+    for k in range(0, len(op.near_src), 7):
+        x = np.searchsorted(op.near_rowptr, k, side="right") - 1
+        y = op.near_src[k]
+        nx, ny = op.size(x), op.size(y)
+        a = op.mat(op.near_off[k], nx, ny)
+        b = nop.mat(nop.near_off[k], nx, ny)
+        assert np.array_equal(a, b)
+
+
+def test_unknown_variant_and_kernel():
+    pts = uniform_points(100, 2, 1)
+    with pytest.raises(ValueError, match="unknown variant"):
+        build_variant("nope", pts)
+    with pytest.raises(ValueError, match="unknown kernel"):
+        build_variant("h2star-bt", pts, kernel="nope")
+
+
+def test_deterministic_and_thread_independent():
+    pts = uniform_points(3000, 2, 5)
+    a = build_variant("h2star-bt", pts, "log2d", 32, 1e-8, n_threads=1)
+    b = build_variant("h2star-bt", pts, "log2d", 32, 1e-8, n_threads=4)
+    assert np.array_equal(a.blob[:len(b.blob)], b.blob[:len(a.blob)])
+    assert a.mem_scalars == b.mem_scalars
+
+
+def test_jittered_grid_generator():
+    """Config 5's points: cell-centred grid (points.py:34-38) + U(-h/2, h/2)."""
+    n = 8
+    p = jittered_grid(n, 3, seed=42)
+    assert p.shape == (n ** 3, 3)
+    h = 2.0 / n
+    centres = -1.0 + (np.floor((p + 1.0) / h) + 0.5) * h
+    assert np.all(np.abs(p - centres) <= 0.5 * h + 1e-15)
+    assert p.min() >= -1.0 and p.max() <= 1.0
