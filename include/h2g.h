@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define H2G_ABI_VERSION 1
+#define H2G_ABI_VERSION 2
 
 enum {
   H2G_OK = 0,
@@ -82,7 +82,9 @@ typedef struct h2g_export_desc {
   const int64_t* blr_rowptr;  /* [n_clusters + 1] */
   const int32_t* blr_src;     /* [nnz] */
   const int32_t* blr_rank;    /* [nnz] p */
-  const int64_t* blr_u_off;   /* [nnz] U: n_X x p column-major */
+  const int64_t* blr_u_off;   /* [nnz] U: n_X x p LEAF-BLOCKED: the rows of leaf L in X
+                                 form an n_L x p column-major block at
+                                 blr_u_off + (cl_start[L] - cl_start[X]) * p */
   const int64_t* blr_v_off;   /* [nnz] V: n_Y x p row-major (= V^T column-major) */
   /* near field (engine.py:260-268): CSR by target leaf */
   const int64_t* near_rowptr; /* [n_clusters + 1] */

@@ -11,7 +11,7 @@ import os
 
 LIBDIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 
-H2G_ABI_VERSION = 1
+H2G_ABI_VERSION = 2
 H2G_OK = 0
 H2G_ERR_LENGTH_MISMATCH = 1
 

@@ -917,7 +917,19 @@ int build_impl(const h2b_params* P, h2b_result** out) {
       const int64_t nx = (int64_t)a.us[0].size(), ny = (int64_t)a.vs[0].size();
       double* U = blob.data() + blr_u[kk];
       double* V = blob.data() + blr_v[kk];
-      for (int64_t c = 0; c < p; ++c) std::memcpy(U + c * nx, a.us[c].data(), nx * sizeof(double));
+      // leaf-blocked U (h2g.h): rows of each leaf L of X form one n_L x p
+      // column-major block at (cl_start[L] - cl_start[X]) * p
+      const int64_t x = blr_x[kk];
+      const int lx = T.level_of(x);
+      const int shift = T.d * (T.kappa - lx);
+      const int64_t first = T.lo[T.kappa] + ((x - T.lo[lx]) << shift);
+      for (int64_t L = first; L < first + (1LL << shift); ++L) {
+        const int64_t r0 = T.st[L] - T.st[x], nl = T.size(L);
+        double* B = U + r0 * p;
+        for (int64_t c = 0; c < p; ++c)
+          std::memcpy(B + c * nl, a.us[c].data() + r0, nl * sizeof(double));
+      }
+      (void)nx;
       for (int64_t r = 0; r < ny; ++r)
         for (int64_t c = 0; c < p; ++c) V[r * p + c] = a.vs[c][r];
     }

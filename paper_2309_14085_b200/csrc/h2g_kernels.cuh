@@ -27,18 +27,13 @@ struct Task {          // 24 bytes
   int32_t pad;
 };
 
-struct Term {          // 24 bytes
-  int64_t a_off;       // blob offset (doubles) of A(0, 0)
+struct Term {          // 32 bytes
+  int64_t a_off;       // offset (doubles) of A(0, 0) in the blob (a_space 0) or arena (1)
   int64_t x_off;       // arena slot of x[0]
   int32_t lda;         // column stride of A in doubles
   int32_t ncols;
-};
-
-struct ReduceJob {     // BLR split-K partials -> w, fixed order
-  int64_t w_off;
-  int64_t part_off;    // partials: chunk c at part_off + c * p
-  int32_t p;
-  int32_t chunks;
+  int32_t a_space;     // 0: operator blob, 1: coefficient arena (split-K partials)
+  int32_t pad;
 };
 
 constexpr int kMaxJ = 8;         // rows per lane -> m <= 256 per task
@@ -89,8 +84,8 @@ __device__ __forceinline__ void run_task(const Task& tk, const Term* __restrict_
   for (int j = 0; j < J; ++j) acc[j] = 0.0;
   for (int t = tk.t_begin; t < tk.t_end; ++t) {
     const Term tm = terms[t];
-    term_accumulate<J>(blob + tm.a_off, tm.lda, tm.ncols, arena + tm.x_off, tk.m, lane, warp,
-                       acc);
+    term_accumulate<J>((tm.a_space ? arena : blob) + tm.a_off, tm.lda, tm.ncols, arena + tm.x_off,
+                       tk.m, lane, warp, acc);
   }
 #pragma unroll
   for (int j = 0; j < J; ++j) red[warp * (32 * J) + lane + 32 * j] = acc[j];
@@ -134,20 +129,6 @@ __global__ void scatter_perm_kernel(const double* __restrict__ in,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     phi[(int64_t)perm[i] * ld] = in[i];
-}
-
-// w[i] = sum_c part[c * p + i], c ascending (deterministic split-K reduce)
-__global__ void reduce_partials_kernel(const ReduceJob* __restrict__ jobs, int n_jobs,
-                                       double* arena) {
-  const int j = blockIdx.x;
-  if (j >= n_jobs) return;
-  const ReduceJob jb = jobs[j];
-  for (int i = threadIdx.x; i < jb.p; i += blockDim.x) {
-    const double* part = arena + jb.part_off + i;
-    double s = 0.0;
-    for (int c = 0; c < jb.chunks; ++c) s += part[(int64_t)c * jb.p];
-    arena[jb.w_off + i] = s;
-  }
 }
 
 }  // namespace h2g

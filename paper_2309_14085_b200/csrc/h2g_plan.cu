@@ -8,8 +8,8 @@
 //   ---------------  -----------------------------  --------------------------------------
 //   gather           q[X.index_set]                 q_tree = q[perm]
 //   up_leaf          P2M   engine.py:194-197        v_ch[X] = P2M_X q_tree[X]   (all channels)
-//                    BLR   blr.py:83 (V^H q)        w_XY (or a split-K chunk) = V^T q_tree[Y]
-//   blr_reduce       (split-K partials, fixed order)
+//   blr_vq           BLR   blr.py:83 (V^H q)        w_XY (or a split-K partial) = V^T q_tree[Y]
+//   (first m2m)      split-K reduce tasks: w_XY = [partials] * ones (fixed order)
 //   m2m_l (l=k-1..1) M2M   engine.py:198-208        v[X] = sum_c M2M_Xc v[c]
 //   down_l (l=1..k)  M2L   engine.py:209-220        u[X] = sum_Y M2L_XY v[Y] + L2L_X u[parent(X)]
 //                    L2L   engine.py:221-228          (L2L fused as the last term)
@@ -53,12 +53,12 @@ int fail(int code, const std::string& msg) {
                   std::string(#expr) + ": " + cudaGetErrorString(_e));               \
   } while (0)
 
-enum PhaseKind { PH_GEMV = 0, PH_REDUCE = 1 };
+enum PhaseKind { PH_GEMV = 0 };
 
 struct Phase {
   int kind;
   std::string name;
-  int64_t task_begin = 0, task_end = 0;  // into d_tasks (GEMV) or d_jobs (REDUCE)
+  int64_t task_begin = 0, task_end = 0;  // into d_tasks
   int64_t alg_bytes = 0;                 // operator + vector bytes (algorithmic)
   int64_t cta_off = 0;                   // streaming engine: CTA ranges at d_cta[cta_off ..]
   int32_t n_cta = 0;
@@ -67,16 +67,16 @@ struct Phase {
 struct HostSchedule {
   std::vector<Task> tasks;
   std::vector<Term> terms;
-  std::vector<ReduceJob> jobs;
   std::vector<Phase> phases;
   // terms of the task currently being built (before row splitting)
   std::vector<Term> cur;
 };
 
-constexpr int kBlrChunkDoubles = 16384;  // split-K chunk of a BLR V^T q product
+constexpr int kBlrChunkDoubles = 65536;  // split-K piece of a BLR V^T q product (512 KB)
 
 struct HostChunk {      // streaming chunk before decoding into a ChunkRec
-  int64_t a_off;        // blob offset (doubles) of the first operator entry
+  int64_t a_off;        // offset (doubles) of the first operator entry (blob or arena)
+  int32_t a_space;      // 0: blob, 1: arena
   int64_t y_off;        // arena slot of y[0] of the owning task
   int32_t lda;          // == m: contiguous run (one copy); else per-column copies
   int32_t m;
@@ -100,6 +100,7 @@ struct h2g_plan {
   int64_t mem_scalars = 0;
   int64_t n_slots = 0;
   int64_t q_tree = 0, phi_tree = 0;
+  int64_t ones_off = 0, n_ones = 0;
   cudaStream_t stream = nullptr;
   double* d_blob = nullptr;
   int64_t blob_len = 0;
@@ -107,7 +108,6 @@ struct h2g_plan {
   int32_t* d_perm = nullptr;
   Task* d_tasks = nullptr;
   Term* d_terms = nullptr;
-  ReduceJob* d_jobs = nullptr;
   std::vector<Phase> phases;
   int64_t n_tasks = 0, n_terms = 0;
   ChunkRec* d_recs = nullptr;
@@ -146,13 +146,16 @@ void emit_task(HostSchedule& s, int64_t y_off, int64_t m, int64_t& bytes) {
   s.cur.clear();
 }
 
-void add_term(HostSchedule& s, int64_t a_off, int64_t x_off, int64_t lda, int64_t ncols) {
+void add_term(HostSchedule& s, int64_t a_off, int64_t x_off, int64_t lda, int64_t ncols,
+              int a_space = 0) {
   if (ncols <= 0) return;
   Term t;
   t.a_off = a_off;
   t.x_off = x_off;
   t.lda = (int32_t)lda;
   t.ncols = (int32_t)ncols;
+  t.a_space = a_space;
+  t.pad = 0;
   s.cur.push_back(t);
 }
 
@@ -160,13 +163,13 @@ void begin_phase(HostSchedule& s, int kind, const std::string& name) {
   Phase p;
   p.kind = kind;
   p.name = name;
-  p.task_begin = kind == PH_GEMV ? (int64_t)s.tasks.size() : (int64_t)s.jobs.size();
+  p.task_begin = (int64_t)s.tasks.size();
   s.phases.push_back(p);
 }
 
 void end_phase(HostSchedule& s) {
   Phase& p = s.phases.back();
-  p.task_end = p.kind == PH_GEMV ? (int64_t)s.tasks.size() : (int64_t)s.jobs.size();
+  p.task_end = (int64_t)s.tasks.size();
   if (p.task_end == p.task_begin) s.phases.pop_back();  // nothing to run
 }
 
@@ -246,6 +249,7 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
   std::vector<int64_t> part_off(blr_nnz, -1);
   std::vector<int32_t> n_chunks(blr_nnz, 1);
   std::vector<int64_t> chunk_cols(blr_nnz, 0);
+  int64_t max_parts = 0;
   for (int64_t k = 0; k < blr_nnz; ++k) {
     const int64_t pr = d->blr_rank[k];
     const int64_t ny = nsz(d->blr_src[k]);
@@ -256,8 +260,13 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
       n_chunks[k] = (int32_t)nch;
       part_off[k] = slots;
       slots += nch * pr;
+      max_parts = std::max(max_parts, nch);
     }
   }
+  const int64_t ones_off = slots;  // ones(max_parts): x of the split-K reduce tasks
+  slots += max_parts;
+  p->ones_off = ones_off;
+  p->n_ones = max_parts;
   p->n_slots = slots;
 
   // ---- up_leaf: P2M of every channel + BLR stage 1 (V^T q) ----
@@ -273,7 +282,12 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
       emit_task(s, v_off[ch][x], c.r_out[x], bytes);
     }
   }
-  std::vector<ReduceJob> jobs;
+  s.phases.back().alg_bytes = bytes;
+  end_phase(s);
+
+  // ---- blr_vq: BLR stage 1, w_XY = V_XY^T q_Y (split-K partials for long Y) ----
+  begin_phase(s, PH_GEMV, "blr_vq");
+  bytes = 0;
   for (int64_t k = 0; k < blr_nnz; ++k) {
     const int64_t y = d->blr_src[k];
     const int64_t pr = d->blr_rank[k];
@@ -292,33 +306,30 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
         add_term(s, d->blr_v_off[k] + c0 * pr, p->q_tree + st[y] + c0, pr, ncols);
         emit_task(s, part_off[k] + ci * pr, pr, bytes);
       }
-      ReduceJob j;
-      j.w_off = w_off[k];
-      j.part_off = part_off[k];
-      j.p = (int32_t)pr;
-      j.chunks = n_chunks[k];
-      jobs.push_back(j);
     }
   }
   s.phases.back().alg_bytes = bytes;
   end_phase(s);
-
-  if (!jobs.empty()) {
-    begin_phase(s, PH_REDUCE, "blr_reduce");
-    int64_t rb = 0;
-    for (const ReduceJob& j : jobs) {
-      s.jobs.push_back(j);
-      rb += 8LL * j.p * (j.chunks + 1);
+  // split-K reduce tasks w = [partial_0 .. partial_C-1] * ones, emitted into
+  // the next launched phase (they only need blr_vq to have finished)
+  auto emit_blr_reduce = [&]() {
+    int64_t scratch = 0;
+    for (int64_t k = 0; k < blr_nnz; ++k) {
+      if (n_chunks[k] == 1) continue;
+      add_term(s, part_off[k], ones_off, d->blr_rank[k], n_chunks[k], /*a_space=*/1);
+      emit_task(s, w_off[k], d->blr_rank[k], scratch);
     }
-    s.phases.back().alg_bytes = 0;  // workspace traffic, not operator bytes
-    (void)rb;
-    end_phase(s);
-  }
+  };
+  bool reduce_pending = blr_nnz > 0;
 
   // ---- upward: M2M levels kappa-1 .. 1 ----
   for (int l = kappa - 1; l >= 1; --l) {
     begin_phase(s, PH_GEMV, "m2m_l" + std::to_string(l));
     bytes = 0;
+    if (reduce_pending) {
+      emit_blr_reduce();
+      reduce_pending = false;
+    }
     for (int ch = 0; ch < d->n_channels; ++ch) {
       const h2g_channel_desc& c = d->channels[ch];
       for (int64_t x = lo[l]; x < lo[l + 1]; ++x) {
@@ -341,6 +352,10 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
   for (int l = 1; l <= kappa; ++l) {
     begin_phase(s, PH_GEMV, "down_l" + std::to_string(l));
     bytes = 0;
+    if (reduce_pending) {  // kappa == 1: no m2m phase
+      emit_blr_reduce();
+      reduce_pending = false;
+    }
     for (int ch = 0; ch < d->n_channels; ++ch) {
       const h2g_channel_desc& c = d->channels[ch];
       for (int64_t x = lo[l]; x < lo[l + 1]; ++x) {
@@ -387,7 +402,8 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
     int64_t a = x;
     for (int l = kappa; l >= 1; --l) {
       for (int64_t k = d->blr_rowptr[a]; k < d->blr_rowptr[a + 1]; ++k)
-        add_term(s, d->blr_u_off[k] + (st[x] - st[a]), w_off[k], nsz(a), d->blr_rank[k]);
+        add_term(s, d->blr_u_off[k] + (st[x] - st[a]) * d->blr_rank[k], w_off[k], nx,
+                 d->blr_rank[k]);  // leaf-blocked U: rows of x are one n_x x p block
       if (l > 1) a = parent(a, l);
     }
     for (int64_t k = d->near_rowptr[x]; k < d->near_rowptr[x + 1]; ++k) {
@@ -440,7 +456,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
           int64_t take;
           const bool x_adjacent =
               open && !segs.empty() && segs.back().x_off + segs.back().ncols == tm.x_off + c0;
-          if (open && !strided && a_here == a_end &&
+          if (open && !strided && a_here == a_end && chunks.back().a_space == tm.a_space &&
               (chunks.back().n_seg < kMaxSeg || x_adjacent) && chunks.back().ncols < per_open) {
             take = std::min<int64_t>(tm.ncols - c0, per_open - chunks.back().ncols);
             if (x_adjacent) {  // x continues the previous segment: one copy serves both
@@ -455,6 +471,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
             take = std::min<int64_t>(tm.ncols - c0, per);
             HostChunk c;
             c.a_off = a_here;
+            c.a_space = tm.a_space;
             c.y_off = t.y_off;
             c.lda = tm.lda;
             c.m = t.m;
@@ -516,7 +533,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
 void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& segs,
                   const double* d_blob, const double* d_arena, std::vector<ChunkRec>& recs) {
   recs.resize(chunks.size());
-  const uint64_t blob = (uint64_t)(uintptr_t)d_blob, arena = (uint64_t)(uintptr_t)d_arena;
+  const uint64_t blob0 = (uint64_t)(uintptr_t)d_blob, arena = (uint64_t)(uintptr_t)d_arena;
   auto round16 = [](int64_t b) { return (uint32_t)((b + 15) & ~int64_t(15)); };
   for (size_t i = 0; i < chunks.size(); ++i) {
     const HostChunk& c = chunks[i];
@@ -529,6 +546,7 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
     r.n_seg = c.n_seg;
     uint32_t total = 0;
     int nc = 0;
+    const uint64_t blob = c.a_space ? arena : blob0;
     if (c.ncols > 0) {
       const bool strided = c.lda != c.m;
       if (!strided) {
@@ -579,12 +597,9 @@ int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s) {
   if (ph.kind == PH_GEMV && p->engine == 1) {
     stream_gemv_kernel<<<ph.n_cta, kStreamThreads, kStreamSmem, s>>>(
         p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
-  } else if (ph.kind == PH_GEMV) {
+  } else {
     gemv_tasks_kernel<<<(unsigned)n, kWarps * 32, 0, s>>>(p->d_tasks + ph.task_begin, p->d_terms,
                                                           p->d_blob, p->d_arena);
-  } else {
-    reduce_partials_kernel<<<(unsigned)n, 128, 0, s>>>(p->d_jobs + ph.task_begin, (int)n,
-                                                       p->d_arena);
   }
   CUDA_TRY(cudaGetLastError());
   return H2G_OK;
@@ -619,7 +634,6 @@ void free_plan(h2g_plan* p) {
   cudaFree(p->d_perm);
   cudaFree(p->d_tasks);
   cudaFree(p->d_terms);
-  cudaFree(p->d_jobs);
   cudaFree(p->d_recs);
   cudaFree(p->d_cta);
   if (p->stream) cudaStreamDestroy(p->stream);
@@ -691,20 +705,24 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
     if ((r = upload((void**)&p->d_perm, perm32.data(), sizeof(int32_t) * p->N))) return r;
     if ((r = upload((void**)&p->d_tasks, s.tasks.data(), sizeof(Task) * s.tasks.size()))) return r;
     if ((r = upload((void**)&p->d_terms, s.terms.data(), sizeof(Term) * s.terms.size()))) return r;
-    if ((r = upload((void**)&p->d_jobs, s.jobs.data(), sizeof(ReduceJob) * s.jobs.size()))) return r;
     if ((r = upload((void**)&p->d_cta, cta.data(), sizeof(int64_t) * cta.size()))) return r;
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kStreamSmem));
     // +8 slots of slack: aligned bulk copies of x may read up to 8 bytes past a slice
     CUDA_TRY(cudaMalloc((void**)&p->d_arena, sizeof(double) * (p->n_slots + 8)));
     CUDA_TRY(cudaMemset(p->d_arena, 0, sizeof(double) * (p->n_slots + 8)));
+    if (p->n_ones > 0) {
+      std::vector<double> ones(p->n_ones, 1.0);
+      CUDA_TRY(cudaMemcpy(p->d_arena + p->ones_off, ones.data(), sizeof(double) * p->n_ones,
+                          cudaMemcpyHostToDevice));
+    }
     {
       std::vector<ChunkRec> recs;
       make_records(chunks, segs, p->d_blob, p->d_arena, recs);
       if ((r = upload((void**)&p->d_recs, recs.data(), sizeof(ChunkRec) * recs.size()))) return r;
     }
     p->workspace_bytes = sizeof(double) * p->n_slots + sizeof(Task) * s.tasks.size() +
-                         sizeof(Term) * s.terms.size() + sizeof(ReduceJob) * s.jobs.size() +
+                         sizeof(Term) * s.terms.size() +
                          sizeof(ChunkRec) * chunks.size() + sizeof(int64_t) * cta.size() +
                          sizeof(int32_t) * p->N;
     // capture the fixed middle phases into one CUDA graph

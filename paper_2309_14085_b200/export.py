@@ -108,6 +108,28 @@ def export_channel(tree, ops, blob: BlobWriter) -> PackedChannel:
                          m2l_off=np.asarray(offs, np.int64))
 
 
+def _put_leaf_blocked(blob: BlobWriter, U, tree, X: int) -> int:
+    """U (n_X x p) as consecutive column-major blocks, one per leaf of X in
+    tree order (packed.py: BLR leg layout).  Returns the first offset."""
+    U = np.asarray(U)
+    lo = tree.level_offset
+    l = tree.clusters[X].level
+    kappa, d = tree.kappa, tree.dim
+    shift = d * (kappa - l)
+    first = lo[kappa] + ((X - lo[l]) << shift)
+    r0, off0 = 0, None
+    for L in range(first, first + (1 << shift)):
+        n = len(tree.clusters[L].index_set)
+        if n == 0:
+            continue
+        off = blob.put_raw(np.asarray(U[r0:r0 + n], dtype=np.float64).ravel(order="F"))
+        off0 = off if off0 is None else off0
+        r0 += n
+    if off0 is None:
+        off0 = blob.put_raw(np.zeros(0))
+    return off0
+
+
 def export_rep(rep, with_points: bool = True) -> PackedOperator:
     """Pack a reference ``HierRep`` (engine.py:235-269) for the GPU plan."""
     tree = rep.tree
@@ -135,7 +157,7 @@ def export_rep(rep, with_points: bool = True) -> PackedOperator:
             for y, f in by_x.get(X, []):
                 b_src.append(y)
                 b_rank.append(f.rank)
-                b_u.append(blob.put(f.U))                     # n_X x p, column-major
+                b_u.append(_put_leaf_blocked(blob, f.U, tree, X))  # leaf-blocked U
                 b_v.append(blob.put(np.conj(f.V), order="C"))  # n_Y x p, row-major
             blr_rowptr[X + 1] = len(b_src)
 

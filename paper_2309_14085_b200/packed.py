@@ -26,8 +26,11 @@ Layout (SURVEY.md §8(a')):
   holds l2l[(c, parent(c))]; the M2L coupling is CSR by target cluster
   (``m2l_rowptr``, ``m2l_src`` ascending = lists_fn order, ``m2l_off``).
 * BLR leg (blr.py:21-33): CSR by target cluster over the (X, Y) factors with
-  rank > 0, ``U`` (n_X x p) column-major at ``blr_u_off``, ``V`` (n_Y x p)
-  row-major at ``blr_v_off``.
+  rank > 0.  ``U`` (n_X x p) is stored LEAF-BLOCKED at ``blr_u_off``: for
+  every leaf L inside X (tree order) the rows of L form one n_L x p
+  column-major block starting at ``blr_u_off + (cl_start[L] - cl_start[X]) * p``,
+  so each leaf's share of the factor is one contiguous run.  ``V`` (n_Y x p)
+  is row-major at ``blr_v_off`` (= V^T column-major).
 * near field (engine.py:260-268, 309-318): CSR by target leaf, dense
   n_X x n_Y column-major blocks at ``near_off``.
 """
@@ -38,7 +41,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-SCHEMA = "h2g-export-1"
+SCHEMA = "h2g-export-2"
 ALIGN = 1  # doubles: blocks are packed back to back (TMA bulk copies align down on device)
 
 CHANNEL_FIELDS = ("r_in", "r_out", "p2m_off", "l2p_off", "m2m_off", "l2l_off",
@@ -124,6 +127,23 @@ class PackedOperator:
 
     def mat_rowmajor(self, off: int, rows: int, cols: int) -> np.ndarray:
         return self.blob[off:off + rows * cols].reshape(rows, cols)
+
+    def leaves_of(self, cid: int):
+        """Leaf ids inside cluster cid, in tree order."""
+        lo = self.level_offset
+        l = int(np.searchsorted(lo, cid, side="right")) - 1
+        shift = self.dim * (self.kappa - l)
+        first = int(lo[self.kappa]) + ((cid - int(lo[l])) << shift)
+        return range(first, first + (1 << shift))
+
+    def blr_U(self, k: int, x: int) -> np.ndarray:
+        """Dense n_X x p U factor of BLR entry k (target x) from its leaf blocks."""
+        p = int(self.blr_rank[k])
+        base = int(self.blr_u_off[k])
+        s0 = int(self.cl_start[x])
+        parts = [self.mat(base + (int(self.cl_start[L]) - s0) * p, self.size(L), p)
+                 for L in self.leaves_of(x) if self.size(L)]
+        return np.concatenate(parts, axis=0) if parts else np.zeros((0, p))
 
     @property
     def operator_bytes(self) -> int:
@@ -270,6 +290,14 @@ class BlobWriter:
             self._len += pad
         off = self._len
         flat = np.asarray(M, dtype=np.float64).ravel(order=order)
+        self._parts.append(flat)
+        self._len += flat.size
+        return off
+
+    def put_raw(self, flat: np.ndarray) -> int:
+        """Append a flat run with no alignment padding (continues the previous one)."""
+        off = self._len
+        flat = np.asarray(flat, dtype=np.float64)
         self._parts.append(flat)
         self._len += flat.size
         return off
