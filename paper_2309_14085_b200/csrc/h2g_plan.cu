@@ -62,6 +62,7 @@ struct Phase {
   int64_t alg_bytes = 0;                 // operator + vector bytes (algorithmic)
   int64_t cta_off = 0;                   // streaming engine: CTA ranges at d_cta[cta_off ..]
   int32_t n_cta = 0;
+  int32_t split = 0;                     // 1: all warps per chunk (narrow phase)
 };
 
 struct HostSchedule {
@@ -423,22 +424,27 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
 }
 
 // Cut every task of every GEMV phase into streaming chunks and partition
-// whole tasks over at most n_sm persistent CTAs, balanced by bytes.  Terms of
+// whole tasks over at most n_cta persistent CTAs, balanced by bytes.  Terms of
 // a task whose operator data is contiguous in the blob (lda == m and the next
 // term starts where the previous ends, e.g. the M2L row of one target or the
-// near blocks of one leaf) share chunks, one x segment per term.
-void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
+// near blocks of one leaf) share chunks, one x segment per term (segments
+// whose x slices are adjacent merge).  Inside a CTA each task is owned by one
+// consumer warp (greedy by bytes); the CTA's chunk stream interleaves the
+// warps' queues so that chunk i belongs to warp i % kConsumers, padding with
+// null chunks.
+void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
                   std::vector<HostChunk>& chunks, std::vector<Seg>& segs,
                   std::vector<int64_t>& cta) {
   for (Phase& ph : phases) {
     if (ph.kind != PH_GEMV) continue;
     const int64_t nt = ph.task_end - ph.task_begin;
+    std::vector<HostChunk> pc;  // this phase's chunks in task order
     std::vector<int64_t> task_chunk0(nt + 1);
     std::vector<double> task_cost(nt);
     double total = 0;
     for (int64_t ti = 0; ti < nt; ++ti) {
       const Task& t = s.tasks[ph.task_begin + ti];
-      task_chunk0[ti] = (int64_t)chunks.size();
+      task_chunk0[ti] = (int64_t)pc.size();
       double cost = 0;
       bool open = false;        // current chunk accepts contiguous continuation
       int64_t a_end = -1;       // blob offset right after the current chunk's data
@@ -456,17 +462,17 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
           int64_t take;
           const bool x_adjacent =
               open && !segs.empty() && segs.back().x_off + segs.back().ncols == tm.x_off + c0;
-          if (open && !strided && a_here == a_end && chunks.back().a_space == tm.a_space &&
-              (chunks.back().n_seg < kMaxSeg || x_adjacent) && chunks.back().ncols < per_open) {
-            take = std::min<int64_t>(tm.ncols - c0, per_open - chunks.back().ncols);
+          if (open && !strided && a_here == a_end && pc.back().a_space == tm.a_space &&
+              (pc.back().n_seg < kMaxSeg || x_adjacent) && pc.back().ncols < per_open) {
+            take = std::min<int64_t>(tm.ncols - c0, per_open - pc.back().ncols);
             if (x_adjacent) {  // x continues the previous segment: one copy serves both
               segs.back().ncols += (int32_t)take;
             } else {
               Seg sg{tm.x_off + c0, (int32_t)take, 0};
               segs.push_back(sg);
-              chunks.back().n_seg += 1;
+              pc.back().n_seg += 1;
             }
-            chunks.back().ncols += (int32_t)take;
+            pc.back().ncols += (int32_t)take;
           } else {
             take = std::min<int64_t>(tm.ncols - c0, per);
             HostChunk c;
@@ -480,7 +486,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
             c.seg_begin = (int32_t)segs.size();
             c.n_seg = 1;
             segs.push_back(Seg{tm.x_off + c0, (int32_t)take, 0});
-            chunks.push_back(c);
+            pc.push_back(c);
             cost += 1024.0;
             open = !strided;
             per_open = per;
@@ -491,38 +497,69 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_sm,
         }
         if (strided) open = false;
       }
-      if ((int64_t)chunks.size() == task_chunk0[ti]) {  // no terms: writes zeros
+      if ((int64_t)pc.size() == task_chunk0[ti]) {  // no terms: writes zeros
         HostChunk c{};
         c.y_off = t.y_off;
         c.lda = t.m;
         c.m = t.m;
         c.seg_begin = (int32_t)segs.size();
         c.n_seg = 0;
-        chunks.push_back(c);
+        pc.push_back(c);
         cost += 1024.0;
       }
-      chunks.back().flags |= kLastOfTask;
+      pc.back().flags |= kLastOfTask;
       task_cost[ti] = cost;
       total += cost;
     }
-    task_chunk0[nt] = (int64_t)chunks.size();
-    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(nt, n_sm));
-    ph.cta_off = (int64_t)cta.size();
-    cta.push_back(task_chunk0[0]);
+    task_chunk0[nt] = (int64_t)pc.size();
+    // partition tasks over CTAs by cost
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(nt, n_cta));
+    std::vector<int64_t> cut_at(1, 0);
     double acc = 0;
-    int64_t g = 0;
     for (int64_t ti = 0; ti < nt; ++ti) {
       acc += task_cost[ti];
+      const int64_t g = (int64_t)cut_at.size() - 1;
       const int64_t left_tasks = nt - ti - 1;
       const int64_t left_groups = G - g - 1;
       const bool cut = left_groups > 0 && left_tasks >= 1 &&
                        (acc >= total * (double)(g + 1) / (double)G || left_tasks <= left_groups);
-      if (cut) {
-        cta.push_back(task_chunk0[ti + 1]);
-        ++g;
-      }
+      if (cut) cut_at.push_back(ti + 1);
     }
-    cta.push_back(task_chunk0[nt]);
+    cut_at.push_back(nt);
+    // narrow phase (fewer tasks than consumer warps on the GPU): split mode
+    ph.split = nt < (int64_t)kConsumers * n_cta ? 1 : 0;
+    // per CTA: tasks -> warps (greedy by cost), interleave queues
+    ph.cta_off = (int64_t)cta.size();
+    for (size_t g = 0; g + 1 < cut_at.size(); ++g) {
+      cta.push_back((int64_t)chunks.size());
+      if (ph.split) {  // task order, every warp sees every chunk
+        for (int64_t c = task_chunk0[cut_at[g]]; c < task_chunk0[cut_at[g + 1]]; ++c)
+          chunks.push_back(pc[c]);
+        continue;
+      }
+      std::vector<int64_t> q[kConsumers];
+      double load[kConsumers] = {0};
+      for (int64_t ti = cut_at[g]; ti < cut_at[g + 1]; ++ti) {
+        int w = 0;
+        for (int v = 1; v < kConsumers; ++v)
+          if (load[v] < load[w]) w = v;
+        load[w] += task_cost[ti];
+        for (int64_t c = task_chunk0[ti]; c < task_chunk0[ti + 1]; ++c) q[w].push_back(c);
+      }
+      size_t len = 0;
+      for (int w = 0; w < kConsumers; ++w) len = std::max(len, q[w].size());
+      for (size_t r = 0; r < len; ++r)
+        for (int w = 0; w < kConsumers; ++w) {
+          if (r < q[w].size()) {
+            chunks.push_back(pc[q[w][r]]);
+          } else {
+            HostChunk nul{};  // null chunk: no data, no output
+            nul.seg_begin = 0;
+            chunks.push_back(nul);
+          }
+        }
+    }
+    cta.push_back((int64_t)chunks.size());
     ph.n_cta = (int32_t)(cta.size() - ph.cta_off - 1);
   }
 }
@@ -583,6 +620,9 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
     }
     r.n_copies = nc;
     r.bytes_a = total;
+    int64_t ext = 0;
+    for (int k = 0; k < nc; ++k) ext = std::max<int64_t>(ext, (r.copies[k].dst + r.copies[k].bytes) / 8);
+    r.extent = (int32_t)((ext + 1) & ~int64_t(1));
   }
 }
 
@@ -595,8 +635,12 @@ int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s) {
   const int64_t n = ph.task_end - ph.task_begin;
   if (n <= 0) return H2G_OK;
   if (ph.kind == PH_GEMV && p->engine == 1) {
-    stream_gemv_kernel<<<ph.n_cta, kStreamThreads, kStreamSmem, s>>>(
-        p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
+    if (ph.split)
+      stream_gemv_kernel<true><<<ph.n_cta, kStreamThreads, kStreamSmem, s>>>(
+          p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
+    else
+      stream_gemv_kernel<false><<<ph.n_cta, kStreamThreads, kStreamSmem, s>>>(
+          p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
   } else {
     gemv_tasks_kernel<<<(unsigned)n, kWarps * 32, 0, s>>>(p->d_tasks + ph.task_begin, p->d_terms,
                                                           p->d_blob, p->d_arena);
@@ -706,8 +750,10 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
     if ((r = upload((void**)&p->d_tasks, s.tasks.data(), sizeof(Task) * s.tasks.size()))) return r;
     if ((r = upload((void**)&p->d_terms, s.terms.data(), sizeof(Term) * s.terms.size()))) return r;
     if ((r = upload((void**)&p->d_cta, cta.data(), sizeof(int64_t) * cta.size()))) return r;
-    CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kStreamSmem));
+    CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
+    CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
     // +8 slots of slack: aligned bulk copies of x may read up to 8 bytes past a slice
     CUDA_TRY(cudaMalloc((void**)&p->d_arena, sizeof(double) * (p->n_slots + 8)));
     CUDA_TRY(cudaMemset(p->d_arena, 0, sizeof(double) * (p->n_slots + 8)));

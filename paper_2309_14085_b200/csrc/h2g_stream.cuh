@@ -12,24 +12,31 @@
 //   * every chunk is pre-decoded on the host into a 256-byte RECORD: the
 //     consumer header (rows, columns, smem stride, alignment shift, segment
 //     table) and the exact list of TMA bulk copies (absolute global source,
-//     smem destination, bytes) that stage its operator data;
-//   * one persistent CTA per SM-slot owns a contiguous range of records (whole
-//     tasks, balanced by bytes on the host); kCtasPerSm pipelines per SM;
+//     ring destination, bytes) that stage its operator data;
+//   * one persistent CTA per SM-slot owns a contiguous range of tasks
+//     (balanced by bytes on the host); kCtasPerSm pipelines per SM.  Inside a
+//     CTA every task is OWNED by one consumer warp; the host interleaves the
+//     chunk stream so that chunk i belongs to warp i % kConsumers (null chunks
+//     pad uneven queues);
 //   * warp 0 is the producer: lane 0 bulk-copies records kRecAhead chunks
-//     ahead into a record ring (own mbarriers); for chunk i it waits for a free
-//     data stage, arms the stage mbarrier (arrive.expect_tx) and lane k issues
-//     the record's k-th cp.async.bulk (SASS UBLKCP);
-//   * warps 1..kConsumers consume.  Warp cw owns chunk columns
-//     c = cw + kConsumers*t.  One chunk ahead it loads the x values of its
-//     columns from L2 into registers (latency hidden behind the current
-//     chunk), parks them in a per-warp smem strip, waits for the stage, and
-//     runs a regular loop: LDS.128 broadcast of two x values, one LDS.64 of A
-//     per 32 rows per column, DFMA into per-lane row accumulators (no
-//     cross-lane reduction).  It releases the stage, and at a task's last chunk
-//     the warps' partial sums are reduced in fixed order and y stored once.
+//     ahead into a record ring, allocates each chunk a 16-byte aligned extent
+//     of a byte-addressed data ring (freeing the oldest released chunks), arms
+//     the slot's mbarrier (arrive.expect_tx) and lane k issues the record's
+//     k-th cp.async.bulk (SASS UBLKCP);
+//   * each consumer warp prefetches the x values of its next chunk from L2
+//     into registers while the current one streams in, parks them in its smem
+//     strip, waits for the slot, and runs a regular loop over the chunk's
+//     columns: LDS.128 broadcast of two x values, one LDS.64 of A per 32 rows
+//     per column, DFMA into per-lane row accumulators.  At a task's last chunk
+//     the lanes store y directly: no cross-lane or cross-warp reduction.
 //
-// Determinism: a task lives in one CTA; each warp accumulates its columns in
-// a fixed order; warps are combined in warp order.  No atomics.
+// Narrow phases (few tasks: the coarse tree levels) run in SPLIT mode
+// instead: all consumer warps work on every chunk (warp cw takes columns
+// cw + kConsumers*t) and a task's partial sums are combined across warps in
+// fixed order through shared memory at its last chunk.
+//
+// Determinism: a task is computed by one warp (or by all warps combined in
+// warp order) in a fixed order.  No atomics.
 #pragma once
 #include <cstdint>
 
@@ -42,8 +49,11 @@ namespace h2g {
 #ifndef H2G_CTAS_PER_SM
 #define H2G_CTAS_PER_SM 2
 #endif
-#ifndef H2G_STAGES
-#define H2G_STAGES 3
+#ifndef H2G_RING_DOUBLES
+#define H2G_RING_DOUBLES 12288   // 96 KB data ring per CTA
+#endif
+#ifndef H2G_SLOTS
+#define H2G_SLOTS 16
 #endif
 #ifndef H2G_CHUNK_A
 #define H2G_CHUNK_A 4096
@@ -52,17 +62,19 @@ constexpr int kLastOfTask = 1;
 constexpr int kConsumers = H2G_CONSUMERS;     // consumer warps per CTA
 constexpr int kStreamThreads = 32 * (1 + kConsumers);
 constexpr int kCtasPerSm = H2G_CTAS_PER_SM;   // independent pipelines per SM
-constexpr int kStages = H2G_STAGES;           // data ring depth (per CTA)
-constexpr int kRecRing = 16;                  // record ring depth
+constexpr int kRing = H2G_RING_DOUBLES;       // byte-addressed data ring (doubles, per CTA)
+constexpr int kSlots = H2G_SLOTS;             // max chunks in flight per CTA
+constexpr int kRecRing = 28;                  // record ring depth
 constexpr int kRecAhead = 8;                  // records prefetched ahead of the producer
 constexpr int kChunkA = H2G_CHUNK_A;          // doubles of operator data per chunk (32 KB)
-constexpr int kChunkCols = 64 * kConsumers;   // max columns per chunk (64 per warp)
+constexpr int kChunkCols = 256;               // max columns per chunk
 constexpr int kMaxCopies = 6;                 // operator bulk copies per chunk (record capacity)
 constexpr int kMaxSeg = 9;                    // x segments per chunk
-constexpr int kStageA = kChunkA + 8;          // + alignment slack
 constexpr int kStreamMaxRows = 256;
-constexpr int kXStrip = 64 + 4;               // per-warp x strip (doubles)
-static_assert(kRecRing >= kStages + kRecAhead, "record ring too shallow");
+constexpr int kXStrip = kChunkCols + 8;       // per-warp x strip (doubles)
+constexpr int kXPerLane = kChunkCols / 32;    // x values a lane prefetches
+static_assert(kRecRing >= kSlots + kRecAhead, "record ring too shallow");
+static_assert(kRing >= kChunkA + 8, "ring smaller than one chunk");
 
 struct CopyDesc {       // 16 bytes
   uint64_t src;         // absolute global address (16-byte aligned)
@@ -81,7 +93,7 @@ struct ChunkRec {       // 256 bytes, host-built, TMA-copied into the record rin
   int32_t odd_lda;      // per-column copies whose alignment shift alternates
   int32_t n_copies;     // operator bulk copies
   uint32_t bytes_a;     // sum of operator copy bytes (expect_tx)
-  int32_t pad0;
+  int32_t extent;       // ring space the chunk occupies (doubles, even)
   int16_t seg_c0[kMaxSeg + 1];  // first chunk column of segment k (+ end sentinel)
   int16_t pad1[kMaxSeg + 1];
   uint64_t seg_src[kMaxSeg];    // absolute address of x for segment k's first column
@@ -89,10 +101,9 @@ struct ChunkRec {       // 256 bytes, host-built, TMA-copied into the record rin
 };
 static_assert(sizeof(ChunkRec) == 256, "record layout");
 
-constexpr size_t kStreamSmem = (size_t)kStages * kStageA * 8 +
-                               (size_t)kConsumers * kStreamMaxRows * 8 +
-                               (size_t)kConsumers * kXStrip * 8 + (size_t)kRecRing * 256 +
-                               (size_t)(2 * kStages + kRecRing) * 8;
+constexpr size_t kStreamSmem = (size_t)kRing * 8 + (size_t)kConsumers * kXStrip * 8 +
+                               (size_t)kRecRing * 256 +
+                               (size_t)(2 * kSlots + kRecRing) * 8 + (size_t)kSlots * 4;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -137,9 +148,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // ---------------------------------------------------------------- consumer
-// x of the warp's local columns t = lane and t = lane + 32 (chunk column
-// c = cw + kConsumers * t), loaded from global (L2); 0 past the chunk.
-__device__ __forceinline__ void fetch_x(const ChunkRec& h, int lane, int cw, double* xr) {
+// x of chunk columns c = lane + 32 q (q < kXPerLane), loaded from global (L2);
+// 0 past the chunk.
+__device__ __forceinline__ void fetch_x(const ChunkRec& h, int lane, double* xr) {
+  const int ncols = h.ncols, n_seg = h.n_seg;
+  int c0[kMaxSeg];
+#pragma unroll
+  for (int k = 0; k < kMaxSeg; ++k) c0[k] = h.seg_c0[k];
+#pragma unroll
+  for (int q = 0; q < kXPerLane; ++q) {
+    const int c = lane + 32 * q;
+    xr[q] = 0.0;
+    if (32 * q < ncols) {  // warp-uniform skip of empty groups
+      int k = 0, start = c0[0];
+#pragma unroll
+      for (int j = 1; j < kMaxSeg; ++j)
+        if (j < n_seg && c >= c0[j]) {  // segments are ascending: the last hit wins
+          k = j;
+          start = c0[j];
+        }
+      if (c < ncols) xr[q] = __ldg(reinterpret_cast<const double*>(h.seg_src[k]) + (c - start));
+    }
+  }
+}
+
+// SPLIT mode: x of the warp's columns c = cw + kConsumers * (lane + 32 q), q < 2.
+__device__ __forceinline__ void fetch_x_split(const ChunkRec& h, int lane, int cw, double* xr) {
   const int ncols = h.ncols, n_seg = h.n_seg;
   int c0[kMaxSeg];
 #pragma unroll
@@ -150,7 +184,7 @@ __device__ __forceinline__ void fetch_x(const ChunkRec& h, int lane, int cw, dou
     int k = 0, start = c0[0];
 #pragma unroll
     for (int j = 1; j < kMaxSeg; ++j)
-      if (j < n_seg && c >= c0[j]) {  // segments are ascending: the last hit wins
+      if (j < n_seg && c >= c0[j]) {
         k = j;
         start = c0[j];
       }
@@ -158,11 +192,11 @@ __device__ __forceinline__ void fetch_x(const ChunkRec& h, int lane, int cw, dou
   }
 }
 
-// One chunk: warp cw owns columns c = cw + kConsumers * t, t < T.  xs holds the
-// x values of those columns (xs[t]); column t at As + t * kConsumers * ldas.
+// One chunk: T columns of one warp, column t at As + t * step, x at xs[t]
+// (owned mode: step = ldas, all columns; split mode: step = kConsumers*ldas).
 // Rows >= m are computed from whatever lies in shared memory and discarded.
 template <int J>
-__device__ __forceinline__ void consume_stage(const double* __restrict__ As, int ldas, int T,
+__device__ __forceinline__ void consume_stage(const double* __restrict__ As, int step, int T,
                                               const double* __restrict__ xs, int lane,
                                               double* acc) {
   constexpr int U = J == 1 ? 8 : (J == 2 ? 4 : 2);  // columns in flight per iteration
@@ -172,7 +206,6 @@ __device__ __forceinline__ void consume_stage(const double* __restrict__ As, int
 #pragma unroll
     for (int j = 0; j < J; ++j) r[u][j] = 0.0;
   const double* base = As + lane;
-  const int step = kConsumers * ldas;
   int t = 0;
   for (; t + U <= T; t += U) {
     double xv[U], a[U][J];
@@ -208,17 +241,18 @@ __device__ __forceinline__ void consume_stage(const double* __restrict__ As, int
   }
 }
 
+template <bool SPLIT>
 __global__ void __launch_bounds__(kStreamThreads, kCtasPerSm)
 stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__ cta_begin,
                    double* arena) {
   extern __shared__ __align__(128) double smem[];
-  double* stage_buf = smem;
-  double* red = smem + (size_t)kStages * kStageA;
-  double* xstrip = red + kConsumers * kStreamMaxRows;
+  double* ring = smem;
+  double* xstrip = smem + kRing;
   ChunkRec* rring = reinterpret_cast<ChunkRec*>(xstrip + kConsumers * kXStrip);
   uint64_t* full = reinterpret_cast<uint64_t*>(rring + kRecRing);
-  uint64_t* empty = full + kStages;
-  uint64_t* recbar = empty + kStages;
+  uint64_t* empty = full + kSlots;
+  uint64_t* recbar = empty + kSlots;
+  int* slot_off = reinterpret_cast<int*>(recbar + kRecRing);  // ring offset of slot's chunk
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -227,9 +261,9 @@ stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict_
   const ChunkRec* my = recs + cb;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kSlots; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers);
+      mbar_init(&empty[s], SPLIT ? kConsumers : 1);  // owning warp, or all warps
     }
     for (int r = 0; r < kRecRing; ++r) mbar_init(&recbar[r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -238,32 +272,64 @@ stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict_
 
   if (warp == 0) {
     // ------------------------------------------------ producer warp
+    // Chunks occupy variable-size, 16-byte aligned extents of the data ring in
+    // issue order; chunk i uses slot i % kSlots.  Lane 0 allocates: it frees
+    // the oldest chunks (waiting for their release) until the next extent fits.
+    int oldest = 0;        // oldest chunk not yet known to be released
+    int head = 0;          // next free ring offset (doubles)
+    int tail = 0;          // ring offset of chunk `oldest` (valid if oldest < i)
     if (lane == 0)
       for (int j = 0; j < kRecAhead && j < n; ++j) {
         mbar_arrive_expect_tx(&recbar[j], sizeof(ChunkRec));
         bulk_g2s(&rring[j], my + j, sizeof(ChunkRec), &recbar[j]);
       }
     for (int i = 0; i < n; ++i) {
-      const int s = i % kStages;
+      const int s = i % kSlots;
       const int r = i % kRecRing;
+      mbar_wait(&recbar[r], (uint32_t)(i / kRecRing) & 1u);
+      const ChunkRec& h = rring[r];
+      int off = 0;
       if (lane == 0) {
-        mbar_wait(&empty[s], ((uint32_t)(i / kStages) & 1u) ^ 1u);
-        // consumers are done with chunk i - kStages; record slot (i + kRecAhead)
-        // % kRecRing last held chunk i + kRecAhead - kRecRing <= i - kStages
+        const int need = h.extent;
+        auto release_oldest = [&]() {
+          mbar_wait(&empty[oldest % kSlots], (uint32_t)(oldest / kSlots) & 1u);
+          ++oldest;
+          tail = oldest < i ? slot_off[oldest % kSlots] : head;
+        };
+        while (i - oldest >= kSlots) release_oldest();
+        while (true) {
+          if (oldest == i) {  // ring empty
+            head = tail = 0;
+            off = 0;
+            break;
+          }
+          // strict inequalities when allocating below `tail` keep head < tail
+          // afterwards, so head == tail never means "full"
+          if (head >= tail) {  // occupied [tail, head): free [head, kRing) and [0, tail)
+            if (kRing - head >= need) { off = head; break; }
+            if (tail > need) { off = 0; break; }
+          } else if (tail - head > need) {  // occupied wraps: free [head, tail)
+            off = head;
+            break;
+          }
+          release_oldest();
+        }
+        head = off + need;
+        slot_off[s] = off;
+        // records ahead: slot (i + kRecAhead) % kRecRing last held chunk
+        // i + kRecAhead - kRecRing < oldest, which consumers have released
         const int j = i + kRecAhead;
         if (j < n) {
           const int rj = j % kRecRing;
           mbar_arrive_expect_tx(&recbar[rj], sizeof(ChunkRec));
           bulk_g2s(&rring[rj], my + j, sizeof(ChunkRec), &recbar[rj]);
         }
+        mbar_arrive_expect_tx(&full[s], h.bytes_a);
       }
-      mbar_wait(&recbar[r], (uint32_t)(i / kRecRing) & 1u);
-      const ChunkRec& h = rring[r];
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], h.bytes_a);
-      __syncwarp();
+      off = __shfl_sync(0xffffffffu, off, 0);
       if (lane < h.n_copies) {  // lane k issues operator copy k (TMA bulk)
         const CopyDesc cd = h.copies[lane];
-        char* st = reinterpret_cast<char*>(stage_buf + (size_t)s * kStageA);
+        char* st = reinterpret_cast<char*>(ring + off);
         bulk_g2s(st + cd.dst, reinterpret_cast<const void*>(cd.src), cd.bytes, &full[s]);
       }
       __syncwarp();
@@ -277,13 +343,91 @@ stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict_
   double acc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-  double xn[2] = {0.0, 0.0};
-  if (n > 0) {
-    mbar_wait(&recbar[0], 0u);
-    fetch_x(rring[0], lane, cw, xn);
+  if constexpr (SPLIT) {
+    // all warps on every chunk; task partials combined across warps in smem
+    // (warp w's strip doubles as its reduction row once its chunk is consumed)
+    double xn[2] = {0.0, 0.0};
+    if (n > 0) {
+      mbar_wait(&recbar[0], 0u);
+      fetch_x_split(rring[0], lane, cw, xn);
+    }
+    for (int i = 0; i < n; ++i) {
+      const int s = i % kSlots;
+      const ChunkRec& h = rring[i % kRecRing];
+      const int m = h.m;
+      const int ncols = h.ncols;
+      const int flags = h.flags;
+      const int ldas = h.ldas;
+      const int a_shift = h.a_shift;
+      const int odd = h.odd_lda;
+      const int64_t y_off = h.y_off;
+      xs[lane] = xn[0];
+      xs[lane + 32] = xn[1];
+      if (i + 1 < n) {
+        mbar_wait(&recbar[(i + 1) % kRecRing], (uint32_t)((i + 1) / kRecRing) & 1u);
+        fetch_x_split(rring[(i + 1) % kRecRing], lane, cw, xn);
+      }
+      __syncwarp();
+      mbar_wait(&full[s], (uint32_t)(i / kSlots) & 1u);
+      const double* sA = ring + slot_off[s];
+      const int T = ncols > cw ? (ncols - cw + kConsumers - 1) / kConsumers : 0;
+#ifndef H2G_DIAG_NOCOMPUTE
+      if (!odd) {
+        const double* As = sA + a_shift + cw * ldas;
+        const int step = kConsumers * ldas;
+        const int J = (m + 31) >> 5;
+        if (J == 1)
+          consume_stage<1>(As, step, T, xs, lane, acc);
+        else if (J == 2)
+          consume_stage<2>(As, step, T, xs, lane, acc);
+        else if (J <= 4)
+          consume_stage<4>(As, step, T, xs, lane, acc);
+        else
+          consume_stage<8>(As, step, T, xs, lane, acc);
+      } else {
+        for (int t = 0; t < T; ++t) {
+          const int c = cw + kConsumers * t;
+          const double* col = sA + (size_t)c * ldas + ((a_shift + c) & 1);
+          const double xv = xs[t];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int rr = lane + 32 * j;
+            if (rr < m) acc[j] = fma(col[rr], xv, acc[j]);
+          }
+        }
+      }
+#endif
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (flags & kLastOfTask) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int rr = lane + 32 * j;
+          if (rr < m) xs[rr] = acc[j];
+          acc[j] = 0.0;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
+        double* y = arena + y_off;
+        for (int rr = threadIdx.x - 32; rr < m; rr += kConsumers * 32) {
+          double sum = xstrip[rr];
+#pragma unroll
+          for (int w = 1; w < kConsumers; ++w) sum += xstrip[w * kXStrip + rr];
+          y[rr] = sum;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
+      }
+    }
+  } else {
+  // owned mode: chunk i belongs to warp i % kConsumers
+  double xn[kXPerLane];
+#pragma unroll
+  for (int q = 0; q < kXPerLane; ++q) xn[q] = 0.0;
+  if (cw < n) {
+    mbar_wait(&recbar[cw % kRecRing], (uint32_t)(cw / kRecRing) & 1u);
+    fetch_x(rring[cw % kRecRing], lane, xn);
   }
-  for (int i = 0; i < n; ++i) {
-    const int s = i % kStages;
+  for (int i = cw; i < n; i += kConsumers) {
+    const int s = i % kSlots;
     const ChunkRec& h = rring[i % kRecRing];
     const int m = h.m;
     const int ncols = h.ncols;
@@ -292,35 +436,35 @@ stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict_
     const int a_shift = h.a_shift;
     const int odd = h.odd_lda;
     const int64_t y_off = h.y_off;
-    // park this chunk's x, then issue the next chunk's x loads (used next iteration)
-    xs[lane] = xn[0];
-    xs[lane + 32] = xn[1];
-    if (i + 1 < n) {
-      mbar_wait(&recbar[(i + 1) % kRecRing], (uint32_t)((i + 1) / kRecRing) & 1u);
-      fetch_x(rring[(i + 1) % kRecRing], lane, cw, xn);
+    // park this chunk's x, then issue the next owned chunk's x loads
+#pragma unroll
+    for (int q = 0; q < kXPerLane; ++q)
+      if (32 * q < ncols) xs[lane + 32 * q] = xn[q];
+    const int inext = i + kConsumers;
+    if (inext < n) {
+      mbar_wait(&recbar[inext % kRecRing], (uint32_t)(inext / kRecRing) & 1u);
+      fetch_x(rring[inext % kRecRing], lane, xn);
     }
     __syncwarp();
-    mbar_wait(&full[s], (uint32_t)(i / kStages) & 1u);
-    const double* sA = stage_buf + (size_t)s * kStageA;
-    const int T = ncols > cw ? (ncols - cw + kConsumers - 1) / kConsumers : 0;
+    mbar_wait(&full[s], (uint32_t)(i / kSlots) & 1u);
+    const double* sA = ring + slot_off[s];
 #ifndef H2G_DIAG_NOCOMPUTE
     if (!odd) {
-      const double* As = sA + a_shift + cw * ldas;
+      const double* As = sA + a_shift;
       const int J = (m + 31) >> 5;
       if (J == 1)
-        consume_stage<1>(As, ldas, T, xs, lane, acc);
+        consume_stage<1>(As, ldas, ncols, xs, lane, acc);
       else if (J == 2)
-        consume_stage<2>(As, ldas, T, xs, lane, acc);
+        consume_stage<2>(As, ldas, ncols, xs, lane, acc);
       else if (J <= 4)
-        consume_stage<4>(As, ldas, T, xs, lane, acc);
+        consume_stage<4>(As, ldas, ncols, xs, lane, acc);
       else
-        consume_stage<8>(As, ldas, T, xs, lane, acc);
+        consume_stage<8>(As, ldas, ncols, xs, lane, acc);
     } else {
       // per-column copies with odd lda (rare): alignment shift alternates
-      for (int t = 0; t < T; ++t) {
-        const int c = cw + kConsumers * t;
+      for (int c = 0; c < ncols; ++c) {
         const double* col = sA + (size_t)c * ldas + ((a_shift + c) & 1);
-        const double xv = xs[t];
+        const double xv = xs[c];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int rr = lane + 32 * j;
@@ -331,25 +475,17 @@ stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict_
 #endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    if (flags & kLastOfTask) {
-      // fixed-order cross-warp reduction, one store per output
+    if (flags & kLastOfTask) {  // this warp owns the task: store y directly
+      double* y = arena + y_off;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int rr = lane + 32 * j;
-        if (rr < m) red[cw * kStreamMaxRows + rr] = acc[j];
+        if (rr < m) y[rr] = acc[j];
         acc[j] = 0.0;
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
-      double* y = arena + y_off;
-      for (int rr = threadIdx.x - 32; rr < m; rr += kConsumers * 32) {
-        double sum = red[rr];
-#pragma unroll
-        for (int w = 1; w < kConsumers; ++w) sum += red[w * kStreamMaxRows + rr];
-        y[rr] = sum;
-      }
-      asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
     }
   }
+  }  // owned mode
 }
 
 }  // namespace h2g
