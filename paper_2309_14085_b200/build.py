@@ -30,7 +30,7 @@ TARGETS = {
 CXX = os.environ.get("H2_CXX", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++")
 # no -march=native / -ffast-math: keep IEEE fp64 operation order (no FMA
 # contraction) like numpy's separate ufunc passes in the reference ACA
-CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
+CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off", "-mavx2", "-mno-fma",
             "-I", os.path.join(ROOT, "include")]
 
 

@@ -21,6 +21,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -188,13 +190,62 @@ int first_row(const Kernel& K, const Idx& rows, const Idx& cols) {  // lowrank.p
   return best;
 }
 
-static double dot(const double* a, const double* b, int64_t n) {
+// ACA work is O(r^2 (m + n)); at the coarse tree levels a single ACA spans
+// 10^5..10^6 candidates, so its loops run in parallel over fixed blocks of
+// kBlk entries.  Reductions (dots, argmax) combine per-block partials in block
+// order, so results do not depend on the thread count; for m, n <= kBlk the
+// arithmetic is exactly the sequential loop's.
+constexpr int64_t kBlk = 2048;
+
+template <class F>
+void for_blocks(int64_t n, bool par, F f) {
+  const int64_t nb = (n + kBlk - 1) / kBlk;
+  if (par && nb > 1) {
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < nb; ++b) f(b, b * kBlk, std::min(n, (b + 1) * kBlk));
+  } else {
+    for (int64_t b = 0; b < nb; ++b) f(b, b * kBlk, std::min(n, (b + 1) * kBlk));
+  }
+}
+
+// sum_i a[i] * b[i] with fixed block partials
+double dot_blocked(const double* a, const double* b, int64_t n, bool par) {
+  const int64_t nb = (n + kBlk - 1) / kBlk;
+  std::vector<double> part(std::max<int64_t>(nb, 1), 0.0);
+  for_blocks(n, par, [&](int64_t blk, int64_t b0, int64_t b1) {
+    double s = 0;
+    for (int64_t i = b0; i < b1; ++i) s += a[i] * b[i];
+    part[blk] = s;
+  });
   double s = 0;
-  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  for (int64_t k = 0; k < nb; ++k) s += part[k];
   return s;
 }
 
-AcaOut aca(const Kernel& K, const Idx& rows, const Idx& cols, double eps, bool keep_factors) {
+// first index of max(mask ? 0 : |v|) (numpy argmax semantics); returns (idx, max)
+std::pair<int64_t, double> argmax_masked(const double* v, const char* used, int64_t n, bool par) {
+  const int64_t nb = (n + kBlk - 1) / kBlk;
+  std::vector<std::pair<int64_t, double>> part(std::max<int64_t>(nb, 1), {0, -1.0});
+  for_blocks(n, par, [&](int64_t blk, int64_t b0, int64_t b1) {
+    int64_t jb = b0;
+    double mb = -1.0;
+    for (int64_t j = b0; j < b1; ++j) {
+      const double mv = used[j] ? 0.0 : std::fabs(v[j]);
+      if (mv > mb) {
+        mb = mv;
+        jb = j;
+      }
+    }
+    part[blk] = {jb, mb};
+  });
+  std::pair<int64_t, double> best = part[0];
+  for (int64_t k = 1; k < nb; ++k)
+    if (part[k].second > best.second) best = part[k];
+  return best;
+}
+
+AcaOut aca(const Kernel& K, const Idx& rows, const Idx& cols, double eps, bool keep_factors,
+           bool par = false) {
   AcaOut out;
   const int64_t m = (int64_t)rows.size(), n = (int64_t)cols.size();
   const int64_t max_rank = std::min(m, n);
@@ -206,22 +257,18 @@ AcaOut aca(const Kernel& K, const Idx& rows, const Idx& cols, double eps, bool k
   auto& us = out.us;
   auto& vs = out.vs;
   while (true) {
-    for (int64_t j = 0; j < n; ++j) row[j] = K.entry(rows[i], cols[j]);
-    for (size_t k = 0; k < us.size(); ++k) {
-      const double ui = us[k][i];
-      const double* v = vs[k].data();
-      for (int64_t j = 0; j < n; ++j) row[j] = row[j] - ui * v[j];
-    }
-    used_rows[i] = 1;
-    int64_t jb = 0;
-    double mb = -1.0;
-    for (int64_t j = 0; j < n; ++j) {
-      const double mv = used_cols[j] ? 0.0 : std::fabs(row[j]);
-      if (mv > mb) {
-        mb = mv;
-        jb = j;
+    // residual row i: K[rows[i], cols] - sum_k u_k[i] v_k (k in order, per entry)
+    for_blocks(n, par, [&](int64_t, int64_t b0, int64_t b1) {
+      const int64_t ri = rows[i];
+      for (int64_t j = b0; j < b1; ++j) row[j] = K.entry(ri, cols[j]);
+      for (size_t k = 0; k < us.size(); ++k) {
+        const double ui = us[k][i];
+        const double* v = vs[k].data();
+        for (int64_t j = b0; j < b1; ++j) row[j] = row[j] - ui * v[j];
       }
-    }
+    });
+    used_rows[i] = 1;
+    const auto [jb, mb] = argmax_masked(row.data(), used_cols.data(), n, par);
     const double piv = row[jb];
     if (mb <= 1e-14 * std::max(1.0, std::sqrt(fro2))) {
       int64_t un = -1;
@@ -234,37 +281,32 @@ AcaOut aca(const Kernel& K, const Idx& rows, const Idx& cols, double eps, bool k
       i = un;
       continue;
     }
-    for (int64_t a = 0; a < m; ++a) col[a] = K.entry(rows[a], cols[jb]);
-    for (size_t k = 0; k < us.size(); ++k) {
-      const double vj = vs[k][jb];
-      const double* u = us[k].data();
-      for (int64_t a = 0; a < m; ++a) col[a] = col[a] - vj * u[a];
-    }
-    used_cols[jb] = 1;
     std::vector<double> u(m);
-    for (int64_t a = 0; a < m; ++a) u[a] = col[a] / piv;
-    const double nu = std::sqrt(dot(u.data(), u.data(), m));
-    const double nv = std::sqrt(dot(row.data(), row.data(), n));
+    for_blocks(m, par, [&](int64_t, int64_t b0, int64_t b1) {
+      const int64_t cj = cols[jb];
+      for (int64_t a = b0; a < b1; ++a) col[a] = K.entry(rows[a], cj);
+      for (size_t k = 0; k < us.size(); ++k) {
+        const double vj = vs[k][jb];
+        const double* uk = us[k].data();
+        for (int64_t a = b0; a < b1; ++a) col[a] = col[a] - vj * uk[a];
+      }
+      for (int64_t a = b0; a < b1; ++a) u[a] = col[a] / piv;
+    });
+    used_cols[jb] = 1;
+    const double nu = std::sqrt(dot_blocked(u.data(), u.data(), m, par));
+    const double nv = std::sqrt(dot_blocked(row.data(), row.data(), n, par));
     double cross = 0.0;
     for (size_t k = 0; k < us.size(); ++k)
-      cross += dot(us[k].data(), u.data(), m) * dot(row.data(), vs[k].data(), n);
+      cross += dot_blocked(us[k].data(), u.data(), m, par) *
+               dot_blocked(row.data(), vs[k].data(), n, par);
     fro2 += 2.0 * cross + (nu * nv) * (nu * nv);
     us.push_back(std::move(u));
     vs.push_back(row);
     out.tau.push_back(rows[i]);
     out.sigma.push_back(cols[jb]);
     if (nu * nv <= eps * std::sqrt(fro2) || (int64_t)us.size() >= max_rank) break;
-    const std::vector<double>& ul = us.back();
-    int64_t ib = -1;
-    double mu = 0.0;
-    for (int64_t a = 0; a < m; ++a) {
-      const double mv = used_rows[a] ? 0.0 : std::fabs(ul[a]);
-      if (mv > mu) {
-        mu = mv;
-        ib = a;
-      }
-    }
-    if (ib < 0) {  // masked.max() == 0
+    const auto [ib, mu] = argmax_masked(us.back().data(), used_rows.data(), m, par);
+    if (mu <= 0.0) {  // masked.max() == 0
       int64_t un = -1;
       for (int64_t a = 0; a < m; ++a)
         if (!used_rows[a]) {
@@ -299,9 +341,9 @@ LU make_lu(const Kernel& K, const Idx& r, const Idx& c, bool transpose) {
 
 // engine.py:39-51
 void pivot_pair(const Kernel& K, const Idx& rows, const Idx& cols, double eps, int64_t cid,
-                Idx& tau, Idx& sigma) {
+                Idx& tau, Idx& sigma, bool par = false) {
   for (double te : {eps, eps / 10.0}) {
-    AcaOut a = aca(K, rows, cols, te, false);
+    AcaOut a = aca(K, rows, cols, te, false, par);
     if (a.tau.empty()) {
       tau.clear();
       sigma.clear();
@@ -539,6 +581,22 @@ void finish_ranks(Channel& ch, int64_t nc) {
   }
 }
 
+double now();
+
+// Run body(x, par) for x in [lo, hi): clusters in parallel when the level has
+// enough of them, otherwise one cluster at a time with the ACA loops inside
+// running in parallel (the coarse levels' few, huge candidate sets).
+template <class F>
+void level_loop(int64_t lo, int64_t hi, F body) {
+  const int64_t cnt = hi - lo;
+  if (cnt < 2 * (int64_t)omp_get_max_threads()) {
+    for (int64_t x = lo; x < hi; ++x) body(x, true);
+  } else {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t x = lo; x < hi; ++x) body(x, false);
+  }
+}
+
 // engine.py:54-86
 void select_b2t(const Tree& T, const Kernel& K, Channel& ch, double eps) {
   const int64_t nc = T.nc();
@@ -547,10 +605,10 @@ void select_b2t(const Tree& T, const Kernel& K, Channel& ch, double eps) {
   for (int l = T.kappa; l >= 1; --l) {
     const bool leaf = l == T.kappa;
     std::string err;
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t x = T.lo[l]; x < T.lo[l + 1]; ++x) {
+    const double tl0 = now();
+    level_loop(T.lo[l], T.lo[l + 1], [&](int64_t x, bool par) {
       try {
-        if (L[x].empty()) continue;
+        if (L[x].empty()) return;
         Quad q;
         Idx ti_c, so_c, si_c, to_c;
         if (leaf) {
@@ -581,14 +639,15 @@ void select_b2t(const Tree& T, const Kernel& K, Channel& ch, double eps) {
           si_c = sorted_union(c2);
           to_c = sorted_union(d2);
         }
-        pivot_pair(K, ti_c, si_c, eps, x, q.t_i, q.s_i);
-        pivot_pair(K, to_c, so_c, eps, x, q.t_o, q.s_o);
+        pivot_pair(K, ti_c, si_c, eps, x, q.t_i, q.s_i, par);
+        pivot_pair(K, to_c, so_c, eps, x, q.t_o, q.s_o, par);
         ch.quads[x] = std::move(q);
       } catch (const std::exception& e) {
 #pragma omp critical
         err = e.what();
       }
-    }
+    });
+    if (getenv("H2B_VERBOSE")) fprintf(stderr, "b2t level %d: %.2f s\n", l, now() - tl0);
     if (!err.empty()) throw SingularCross(err);
   }
   finish_ranks(ch, nc);
@@ -601,15 +660,15 @@ void select_t2b(const Tree& T, const Kernel& K, Channel& ch, double eps) {
   const auto& L = *ch.lists;
   for (int l = 1; l <= T.kappa; ++l) {
     std::string err;
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t x = T.lo[l]; x < T.lo[l + 1]; ++x) {
+    const double tl0 = now();
+    level_loop(T.lo[l], T.lo[l + 1], [&](int64_t x, bool par) {
       try {
         const Quad* pq = nullptr;
         if (l >= 2) {
           const Quad& p = ch.quads[T.parent(x, l)];
           if (!p.empty()) pq = &p;
         }
-        if (L[x].empty() && !pq) continue;
+        if (L[x].empty() && !pq) return;
         std::vector<Idx> mem;
         for (int64_t y : L[x]) mem.push_back(T.index_set(y));
         std::vector<const Idx*> a, b;
@@ -625,14 +684,15 @@ void select_t2b(const Tree& T, const Kernel& K, Channel& ch, double eps) {
         const Idx to_c = sorted_union(b);
         const Idx xs = T.index_set(x);
         Quad q;
-        pivot_pair(K, xs, si_c, eps, x, q.t_i, q.s_i);
-        pivot_pair(K, to_c, xs, eps, x, q.t_o, q.s_o);
+        pivot_pair(K, xs, si_c, eps, x, q.t_i, q.s_i, par);
+        pivot_pair(K, to_c, xs, eps, x, q.t_o, q.s_o, par);
         ch.quads[x] = std::move(q);
       } catch (const std::exception& e) {
 #pragma omp critical
         err = e.what();
       }
-    }
+    });
+    if (getenv("H2B_VERBOSE")) fprintf(stderr, "t2b level %d: %.2f s\n", l, now() - tl0);
     if (!err.empty()) throw SingularCross(err);
   }
   finish_ranks(ch, nc);
@@ -841,9 +901,18 @@ int build_impl(const h2b_params* P, h2b_result** out) {
           blr_y.push_back(y);
         }
   std::vector<AcaOut> fac(blr_x.size());
+  {
+    // factors with huge candidate sets (coarse levels): one at a time, ACA
+    // loops in parallel; the rest: factors in parallel
+    const int64_t big = 1 << 16;
+    for (int64_t f = 0; f < (int64_t)blr_x.size(); ++f)
+      if (T.size(blr_x[f]) + T.size(blr_y[f]) > big)
+        fac[f] = aca(K, T.index_set(blr_x[f]), T.index_set(blr_y[f]), P->eps_ver, true, true);
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t f = 0; f < (int64_t)blr_x.size(); ++f)
-    fac[f] = aca(K, T.index_set(blr_x[f]), T.index_set(blr_y[f]), P->eps_ver, true);
+    for (int64_t f = 0; f < (int64_t)blr_x.size(); ++f)
+      if (T.size(blr_x[f]) + T.size(blr_y[f]) <= big)
+        fac[f] = aca(K, T.index_set(blr_x[f]), T.index_set(blr_y[f]), P->eps_ver, true);
+  }
   R->timing["blr"] = now() - t0;
   std::vector<int64_t> blr_rowptr(nc + 1, 0), blr_u, blr_v;
   std::vector<int32_t> blr_src, blr_rank;
