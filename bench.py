@@ -14,8 +14,8 @@ A step is one matvec phi = K~ q.  ``value`` = matvecs/s of the headline
 variant (h2star-bt) over all ranks, device-timed with CUDA events on the
 plan's stream, inputs resident in HBM; the operator (6.6 GB) is far larger
 than L2 (126 MB), so no flush is needed.  ``e2e`` is the same metric through
-the public API (GpuHierRep.matvec on a pinned host vector: H2D copy, matvec,
-D2H copy inside the timed region).  ``roofline`` reports the streaming GEMV
+the public API (GpuHierRep.matvec(q, out=phi) on pinned host vectors: H2D
+copy, matvec, D2H copy inside the timed region).  ``roofline`` reports the streaming GEMV
 kernel's achieved algorithmic bytes/s against MEASURED_PEAKS.json.
 ``cpu_baseline`` times the oracle port of the reference matvec
 (oracle/packed_matvec.py, one core) on a bounded sample.
@@ -173,12 +173,13 @@ def bench_variant(op, args, torch, dev, rank, world):
     # e2e through the public API with pinned host buffers
     q_pin = torch.from_numpy(q).pin_memory()
     qh = q_pin.numpy()
+    phi_pin = torch.empty(N, dtype=torch.float64).pin_memory().numpy()
     phi = None
     for _ in range(max(1, args.warmup // 2)):
-        phi = rep.matvec(qh)
+        phi = rep.matvec(qh, out=phi_pin)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        phi = rep.matvec(qh)
+        phi = rep.matvec(qh, out=phi_pin)
     e2e_s = (time.perf_counter() - t0) / args.steps
     res = {"rep": rep, "ms": ms, "prof": prof, "clk": clk.summary(), "e2e_s": e2e_s,
            "q": q, "phi": phi, "out": out}

@@ -131,4 +131,31 @@ __global__ void scatter_perm_kernel(const double* __restrict__ in,
     phi[(int64_t)perm[i] * ld] = in[i];
 }
 
+// batched RHS: out[i * KB + b] = q[perm[i] * ld + col0 + b] (0 for b >= nb)
+template <int KB>
+__global__ void gather_batch_kernel(const double* __restrict__ q, int64_t ld, int64_t col0,
+                                    int nb, const int32_t* __restrict__ perm,
+                                    double* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* src = q + (int64_t)perm[i] * ld + col0;
+#pragma unroll
+    for (int b = 0; b < KB; ++b) out[i * KB + b] = b < nb ? src[b] : 0.0;
+  }
+}
+
+// batched RHS: phi[perm[i] * ld + col0 + b] = in[i * KB + b] for b < nb
+template <int KB>
+__global__ void scatter_batch_kernel(const double* __restrict__ in,
+                                     const int32_t* __restrict__ perm, double* __restrict__ phi,
+                                     int64_t ld, int64_t col0, int nb, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double* dst = phi + (int64_t)perm[i] * ld + col0;
+#pragma unroll
+    for (int b = 0; b < KB; ++b)
+      if (b < nb) dst[b] = in[i * KB + b];
+  }
+}
+
 }  // namespace h2g

@@ -74,6 +74,7 @@ struct HostSchedule {
 };
 
 constexpr int kBlrChunkDoubles = 65536;  // split-K piece of a BLR V^T q product (512 KB)
+constexpr int kRhsBatch = 8;             // right-hand sides per batched pass
 
 struct HostChunk {      // streaming chunk before decoding into a ChunkRec
   int64_t a_off;        // offset (doubles) of the first operator entry (blob or arena)
@@ -119,6 +120,19 @@ struct h2g_plan {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   int64_t workspace_bytes = 0;
+  // batched-RHS engine (built on first nrhs > 1 call)
+  HostSchedule sched;               // host schedule kept for the batched build
+  std::vector<Phase> phases_b;
+  double* d_arena_b = nullptr;      // n_slots x kRhsBatch
+  ChunkRec* d_recs_b = nullptr;
+  int64_t* d_cta_b = nullptr;
+  cudaGraph_t graph_b = nullptr;
+  cudaGraphExec_t graph_b_exec = nullptr;
+  bool batched_ready = false;
+  bool use_batched = true;  // nrhs > 1 through the batched engine (H2G_BATCHED=0: column loop)
+  double* d_hq = nullptr;    // host-call staging (h2g_matvec_host)
+  double* d_hphi = nullptr;
+  size_t h_cap = 0;
 };
 
 namespace {
@@ -434,7 +448,7 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
 // null chunks.
 void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
                   std::vector<HostChunk>& chunks, std::vector<Seg>& segs,
-                  std::vector<int64_t>& cta) {
+                  std::vector<int64_t>& cta, int kb = 1) {
   for (Phase& ph : phases) {
     if (ph.kind != PH_GEMV) continue;
     const int64_t nt = ph.task_end - ph.task_begin;
@@ -527,7 +541,8 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
     }
     cut_at.push_back(nt);
     // narrow phase (fewer tasks than consumer warps on the GPU): split mode
-    ph.split = nt < (int64_t)kConsumers * n_cta ? 1 : 0;
+    // (single RHS only; the batched engine always runs owned tasks)
+    ph.split = (kb == 1 && nt < (int64_t)kConsumers * n_cta) ? 1 : 0;
     // per CTA: tasks -> warps (greedy by cost), interleave queues
     ph.cta_off = (int64_t)cta.size();
     for (size_t g = 0; g + 1 < cut_at.size(); ++g) {
@@ -568,7 +583,8 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
 // alignment shifts, smem placement and the exact TMA bulk-copy list.  Needs
 // the device base addresses (blob and arena are 256-byte aligned).
 void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& segs,
-                  const double* d_blob, const double* d_arena, std::vector<ChunkRec>& recs) {
+                  const double* d_blob, const double* d_arena, std::vector<ChunkRec>& recs,
+                  int kb = 1) {
   recs.resize(chunks.size());
   const uint64_t blob0 = (uint64_t)(uintptr_t)d_blob, arena = (uint64_t)(uintptr_t)d_arena;
   auto round16 = [](int64_t b) { return (uint32_t)((b + 15) & ~int64_t(15)); };
@@ -613,15 +629,23 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
       for (int k = 0; k < c.n_seg; ++k) {
         const Seg& sg = segs[c.seg_begin + k];
         r.seg_c0[k] = (int16_t)col;
-        r.seg_src[k] = arena + 8 * (uint64_t)sg.x_off;
+        r.seg_src[k] = arena + 8 * (uint64_t)sg.x_off * kb;
         col += sg.ncols;
       }
       r.seg_c0[c.n_seg] = (int16_t)col;
     }
     r.n_copies = nc;
     r.bytes_a = total;
+    if (kb > 1) {  // X (ncols x kb) staged after the operator data, 16-byte aligned
+      int64_t ext = 0;
+      for (int k = 0; k < nc; ++k)
+        ext = std::max<int64_t>(ext, (r.copies[k].dst + r.copies[k].bytes) / 8);
+      r.x_base = (int32_t)((ext + 1) & ~int64_t(1));
+      r.bytes_x = (uint32_t)(8 * (int64_t)kb * c.ncols);
+    }
     int64_t ext = 0;
     for (int k = 0; k < nc; ++k) ext = std::max<int64_t>(ext, (r.copies[k].dst + r.copies[k].bytes) / 8);
+    if (kb > 1) ext = std::max<int64_t>(ext, (int64_t)r.x_base + (int64_t)kb * c.ncols);
     r.extent = (int32_t)((ext + 1) & ~int64_t(1));
   }
 }
@@ -679,6 +703,13 @@ void free_plan(h2g_plan* p) {
   cudaFree(p->d_tasks);
   cudaFree(p->d_terms);
   cudaFree(p->d_recs);
+  if (p->graph_b_exec) cudaGraphExecDestroy(p->graph_b_exec);
+  if (p->graph_b) cudaGraphDestroy(p->graph_b);
+  cudaFree(p->d_arena_b);
+  cudaFree(p->d_recs_b);
+  cudaFree(p->d_cta_b);
+  cudaFree(p->d_hq);
+  cudaFree(p->d_hphi);
   cudaFree(p->d_cta);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
@@ -710,6 +741,8 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
   {
     const char* e = getenv("H2G_ENGINE");
     if (e && std::string(e) == "ldg") p->engine = 0;
+    const char* b = getenv("H2G_BATCHED");
+    if (b && std::string(b) == "0") p->use_batched = false;
     int nsm = 0;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess &&
         nsm > 0)
@@ -722,6 +755,7 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
   p->n_chunks = (int64_t)chunks.size();
   p->phases = s.phases;
   p->n_tasks = (int64_t)s.tasks.size();
+  p->sched = s;
   p->n_terms = (int64_t)s.terms.size();
   if (p->n_terms >= (1LL << 31)) {
     delete p;
@@ -753,6 +787,8 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
+    CUDA_TRY(cudaFuncSetAttribute(stream_gemm_kernel<kRhsBatch>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
     // +8 slots of slack: aligned bulk copies of x may read up to 8 bytes past a slice
     CUDA_TRY(cudaMalloc((void**)&p->d_arena, sizeof(double) * (p->n_slots + 8)));
@@ -797,12 +833,63 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
   return H2G_OK;
 }
 
+// Batched-RHS schedule: the same tasks, cut into chunks whose X (ncols x
+// kRhsBatch) also fits the ring, over an arena of kRhsBatch-wide slots.
+int ensure_batched(h2g_plan* p) {
+  if (p->batched_ready) return H2G_OK;
+  std::vector<HostChunk> chunks;
+  std::vector<int64_t> cta;
+  std::vector<Seg> segs;
+  p->phases_b = p->sched.phases;
+  build_chunks(p->sched, p->phases_b, p->n_sm * kCtasPerSm, chunks, segs, cta, kRhsBatch);
+  const size_t slots = (size_t)(p->n_slots + 8) * kRhsBatch;
+  CUDA_TRY(cudaMalloc((void**)&p->d_arena_b, sizeof(double) * slots));
+  CUDA_TRY(cudaMemset(p->d_arena_b, 0, sizeof(double) * slots));
+  if (p->n_ones > 0) {
+    std::vector<double> ones((size_t)p->n_ones * kRhsBatch, 1.0);
+    CUDA_TRY(cudaMemcpy(p->d_arena_b + (size_t)p->ones_off * kRhsBatch, ones.data(),
+                        sizeof(double) * ones.size(), cudaMemcpyHostToDevice));
+  }
+  std::vector<ChunkRec> recs;
+  make_records(chunks, segs, p->d_blob, p->d_arena_b, recs, kRhsBatch);
+  CUDA_TRY(cudaMalloc((void**)&p->d_recs_b, sizeof(ChunkRec) * recs.size()));
+  CUDA_TRY(cudaMemcpy(p->d_recs_b, recs.data(), sizeof(ChunkRec) * recs.size(),
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc((void**)&p->d_cta_b, sizeof(int64_t) * cta.size()));
+  CUDA_TRY(cudaMemcpy(p->d_cta_b, cta.data(), sizeof(int64_t) * cta.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+  for (const Phase& ph : p->phases_b) {
+    stream_gemm_kernel<kRhsBatch><<<ph.n_cta, kStreamThreads, kStreamSmem, p->stream>>>(
+        p->d_recs_b, p->d_cta_b + ph.cta_off, p->d_arena_b);
+  }
+  CUDA_TRY(cudaStreamEndCapture(p->stream, &p->graph_b));
+  CUDA_TRY(cudaGraphInstantiate(&p->graph_b_exec, p->graph_b, 0));
+  p->workspace_bytes += sizeof(double) * slots + sizeof(ChunkRec) * recs.size();
+  p->batched_ready = true;
+  return H2G_OK;
+}
+
 int matvec_impl(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nrhs, int64_t ld,
                 cudaStream_t s) {
   int rc = check_vec_args(p, n, nrhs, ld);
   if (rc) return rc;
   if (!q || !phi) return fail(H2G_ERR_INVALID_ARG, "null vector");
   CUDA_TRY(cudaSetDevice(p->device));
+  if (nrhs > 1 && p->engine == 1 && p->use_batched) {
+    rc = ensure_batched(p);
+    if (rc) return rc;
+    for (int64_t c0 = 0; c0 < nrhs; c0 += kRhsBatch) {
+      const int nb = (int)std::min<int64_t>(kRhsBatch, nrhs - c0);
+      gather_batch_kernel<kRhsBatch><<<grid_for(n), 256, 0, s>>>(
+          q, ld, c0, nb, p->d_perm, p->d_arena_b + (size_t)p->q_tree * kRhsBatch, n);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaGraphLaunch(p->graph_b_exec, s));
+      scatter_batch_kernel<kRhsBatch><<<grid_for(n), 256, 0, s>>>(
+          p->d_arena_b + (size_t)p->phi_tree * kRhsBatch, p->d_perm, phi, ld, c0, nb, n);
+      CUDA_TRY(cudaGetLastError());
+    }
+    return H2G_OK;
+  }
   for (int64_t j = 0; j < nrhs; ++j) {
     gather_perm_kernel<<<grid_for(n), 256, 0, s>>>(q + j, ld, p->d_perm, p->d_arena + p->q_tree, n);
     CUDA_TRY(cudaGetLastError());
@@ -865,6 +952,8 @@ int h2g_plan_get_stats(const h2g_plan* p, h2g_plan_stats* o) {
 
 int h2g_launches_per_matvec(const h2g_plan* p, int64_t nrhs) {
   if (!p) return 0;
+  if (nrhs > 1 && p->engine == 1 && p->use_batched)
+    return (int)((p->sched.phases.size() + 2) * ((nrhs + kRhsBatch - 1) / kRhsBatch));
   return (int)((p->phases.size() + 2) * (nrhs < 1 ? 1 : nrhs));
 }
 
@@ -879,18 +968,25 @@ int h2g_matvec_host(h2g_plan* p, const double* q_host, double* phi_host, int64_t
   if (rc) return rc;
   if (!q_host || !phi_host) return fail(H2G_ERR_INVALID_ARG, "null vector");
   CUDA_TRY(cudaSetDevice(p->device));
-  const size_t bytes = sizeof(double) * (size_t)n * (size_t)ld;
-  double *dq = nullptr, *dphi = nullptr;
-  CUDA_TRY(cudaMallocAsync((void**)&dq, bytes, p->stream));
-  CUDA_TRY(cudaMallocAsync((void**)&dphi, bytes, p->stream));
+  const size_t elems = (size_t)n * (size_t)ld;
+  const size_t bytes = sizeof(double) * elems;
+  if (p->h_cap < elems) {  // persistent device staging for host-pointer calls
+    cudaFree(p->d_hq);
+    cudaFree(p->d_hphi);
+    p->d_hq = p->d_hphi = nullptr;
+    p->h_cap = 0;
+    CUDA_TRY(cudaMalloc((void**)&p->d_hq, bytes));
+    CUDA_TRY(cudaMalloc((void**)&p->d_hphi, bytes));
+    p->h_cap = elems;
+  }
+  double* dq = p->d_hq;
+  double* dphi = p->d_hphi;
   CUDA_TRY(cudaMemcpyAsync(dq, q_host, bytes, cudaMemcpyHostToDevice, p->stream));
   if (ld != nrhs)  // keep the caller's padding columns intact
     CUDA_TRY(cudaMemcpyAsync(dphi, phi_host, bytes, cudaMemcpyHostToDevice, p->stream));
   rc = matvec_impl(p, dq, dphi, n, nrhs, ld, p->stream);
   if (rc == H2G_OK)
     CUDA_TRY(cudaMemcpyAsync(phi_host, dphi, bytes, cudaMemcpyDeviceToHost, p->stream));
-  cudaFreeAsync(dq, p->stream);
-  cudaFreeAsync(dphi, p->stream);
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   return rc;
 }

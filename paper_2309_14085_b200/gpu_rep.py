@@ -156,11 +156,15 @@ class GpuHierRep:
         return int(self._L.h2g_launches_per_matvec(self._plan, int(nrhs)))
 
     # -------------------------------------------------------------- apply
-    def _apply_host(self, Q: np.ndarray) -> np.ndarray:
-        """Q: (N,) or (N, k) float64 -> same shape."""
+    def _apply_host(self, Q: np.ndarray, out: np.ndarray = None) -> np.ndarray:
+        """Q: (N,) or (N, k) float64 -> same shape (into ``out`` if given)."""
         Q = np.ascontiguousarray(Q, dtype=np.float64)
         k = 1 if Q.ndim == 1 else Q.shape[1]
-        out = np.empty_like(Q)
+        if out is None:
+            out = np.empty_like(Q)
+        elif (out.shape != Q.shape or out.dtype != np.float64
+              or not out.flags.c_contiguous or not out.flags.writeable):
+            raise ValueError("out must be a writable C-contiguous float64 array shaped like q")
         if Q.size == 0:
             return out
         _lib.check(self._L.h2g_matvec_host(self._plan, _ptr(Q, C.c_double), _ptr(out, C.c_double),
@@ -186,8 +190,11 @@ class GpuHierRep:
         torch = _torch()
         return torch is not None and isinstance(q, torch.Tensor)
 
-    def matvec(self, q):
-        """phi = K~ q (HierRep.matvec, engine.py:250-269)."""
+    def matvec(self, q, out=None):
+        """phi = K~ q (HierRep.matvec, engine.py:250-269).
+
+        ``out`` (numpy only, optional): a float64 array to receive phi, e.g. a
+        pinned buffer for full-bandwidth device->host copies; returned."""
         if self._is_torch(q):
             if q.dim() != 1:
                 raise ValueError("matvec expects a 1-D vector (use matmat for blocks)")
@@ -204,8 +211,10 @@ class GpuHierRep:
         if len(q) != self.N:
             raise ValueError("vector length mismatch")
         if np.iscomplexobj(q):
+            if out is not None:
+                raise ValueError("out= is not supported for complex q")
             return self._apply_host(q.real) + 1j * self._apply_host(q.imag)
-        return self._apply_host(q)
+        return self._apply_host(q, out)
 
     def matmat(self, Q):
         """Phi = K~ Q for an N x k block (reference: a column loop of matvec)."""

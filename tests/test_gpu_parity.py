@@ -112,3 +112,16 @@ def test_native_library_is_loaded(reps):
     rep = reps[NAMES[0]][0]
     st = rep.stats()
     assert st["graph"] == 1 and st["n_tasks"] > 0
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_batched_rhs_engine(reps, name):
+    """nrhs > 1 runs the batched engine (each operator chunk read once per 8
+    right-hand sides); every column equals the single-RHS matvec and the
+    oracle (the reference's equivalent is a column loop)."""
+    rep, op, z, meta = reps[name]
+    Q = np.random.default_rng(11).standard_normal((op.N, 13))  # 8 + a ragged batch of 5
+    Phi = rep.matmat(Q)
+    for j in (0, 5, 7, 8, 12):
+        assert rel_err(Phi[:, j], rep.matvec(Q[:, j])) <= 1e-13
+        assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= TOL
