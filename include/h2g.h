@@ -137,6 +137,46 @@ int h2g_profile_phases(h2g_plan* plan, const double* q_dev, double* phi_dev, int
  * SMs (no CUDA calls) and write a JSON summary per phase into buf. */
 int h2g_schedule_info(const h2g_export_desc* desc, int n_sm, char* buf, int64_t buflen);
 
+/* ---- multi-GPU (one process per GPU) ----
+ * Subtrees at level L_s are split into nranks contiguous Morton ranges; rank
+ * r computes the clusters of its subtrees (and the replicated coarse levels)
+ * and the phi rows [row_begin, row_end) of tree order.  q is replicated.
+ * One matvec:  h2g_matvec_begin(q)  ->  h2g_shard_pack(send)  ->
+ * all-gather of send (max_send_slots doubles per rank, rank-major, e.g. NCCL
+ * ncclAllGather) into recv  ->  h2g_shard_unpack(recv)  ->  h2g_matvec_end(phi)
+ * (phi receives this rank's rows only).  A rank uploads only the operator
+ * blocks its tasks read. */
+typedef struct h2g_shard_info {
+  int32_t rank, nranks;
+  int32_t level;               /* L_s */
+  int32_t pad;
+  int64_t row_begin, row_end;  /* owned tree-order rows */
+  int64_t send_slots;          /* doubles this rank contributes to the exchange */
+  int64_t max_send_slots;      /* per-rank stride of the all-gather buffer */
+  int64_t blob_bytes;          /* operator bytes resident on this rank */
+} h2g_shard_info;
+
+int h2g_plan_create_sharded(const h2g_export_desc* desc, int device, int rank, int nranks,
+                            h2g_plan** out);
+int h2g_shard_get_info(const h2g_plan* plan, h2g_shard_info* out);
+int h2g_matvec_begin(h2g_plan* plan, const double* q_dev, int64_t n, void* stream);
+int h2g_shard_pack(h2g_plan* plan, double* send_dev, void* stream);
+int h2g_shard_unpack(h2g_plan* plan, const double* recv_dev, void* stream);
+int h2g_matvec_end(h2g_plan* plan, double* phi_dev, int64_t n, void* stream);
+
+/* Host-only view of rank `rank`'s schedule (no CUDA; emulation and tests):
+ * named int64 arrays "tasks" [n x 4: y_off, m, t_begin, t_end], "terms"
+ * [n x 5: a_off, x_off, lda, ncols, a_space], "phases" [n x 4: task_begin,
+ * task_end, part, alg_bytes], "pack" / "unpack" [n x 3: src, dst, len],
+ * "meta" [n_slots, q_tree, phi_tree, ones_off, n_ones, row_begin, row_end,
+ * send_slots, max_send_slots, level] and the compacted f64 "blob" (empty when
+ * nranks == 1: terms index the export's blob). */
+typedef struct h2g_sched h2g_sched;
+int h2g_schedule_build(const h2g_export_desc* desc, int rank, int nranks, h2g_sched** out);
+int h2g_schedule_get(const h2g_sched* sched, const char* name, const void** ptr, int64_t* len,
+                     int32_t* is_f64);
+void h2g_schedule_free(h2g_sched* sched);
+
 /* Number of kernels a single-RHS matvec launches (for bench gpu_launches). */
 int h2g_launches_per_matvec(const h2g_plan* plan, int64_t nrhs);
 

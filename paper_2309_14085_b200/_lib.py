@@ -44,11 +44,21 @@ class PlanStats(C.Structure):
                 ("n_terms", C.c_int64), ("device", C.c_int32), ("graph", C.c_int32)]
 
 
+class ShardInfo(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("level", C.c_int32),
+                ("pad", C.c_int32), ("row_begin", C.c_int64), ("row_end", C.c_int64),
+                ("send_slots", C.c_int64), ("max_send_slots", C.c_int64),
+                ("blob_bytes", C.c_int64)]
+
+
 # every symbol include/h2g.h declares (checked by tests/test_abi.py)
 H2G_SYMBOLS = ("h2g_plan_create", "h2g_plan_destroy", "h2g_plan_get_stats", "h2g_matvec",
                "h2g_matvec_host", "h2g_profile_phases", "h2g_schedule_info",
                "h2g_launches_per_matvec",
-               "h2g_error_string", "h2g_last_error_detail", "h2g_abi_version")
+               "h2g_error_string", "h2g_last_error_detail", "h2g_abi_version",
+               "h2g_plan_create_sharded", "h2g_shard_get_info", "h2g_matvec_begin",
+               "h2g_shard_pack", "h2g_shard_unpack", "h2g_matvec_end",
+               "h2g_schedule_build", "h2g_schedule_get", "h2g_schedule_free")
 
 _LIB = None
 
@@ -81,6 +91,18 @@ def load(path: str = None) -> C.CDLL:
                                      C.POINTER(C.c_char_p), C.c_int, C.POINTER(C.c_int)]
     L.h2g_launches_per_matvec.argtypes = [vp, C.c_int64]
     L.h2g_schedule_info.argtypes = [C.POINTER(ExportDesc), C.c_int, C.c_char_p, C.c_int64]
+    L.h2g_plan_create_sharded.argtypes = [C.POINTER(ExportDesc), C.c_int, C.c_int, C.c_int,
+                                          C.POINTER(vp)]
+    L.h2g_shard_get_info.argtypes = [vp, C.POINTER(ShardInfo)]
+    L.h2g_matvec_begin.argtypes = [vp, vp, C.c_int64, vp]
+    L.h2g_shard_pack.argtypes = [vp, vp, vp]
+    L.h2g_shard_unpack.argtypes = [vp, vp, vp]
+    L.h2g_matvec_end.argtypes = [vp, vp, C.c_int64, vp]
+    L.h2g_schedule_build.argtypes = [C.POINTER(ExportDesc), C.c_int, C.c_int, C.POINTER(vp)]
+    L.h2g_schedule_get.argtypes = [vp, C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_int32)]
+    L.h2g_schedule_free.argtypes = [vp]
+    L.h2g_schedule_free.restype = None
     L.h2g_error_string.argtypes = [C.c_int]
     L.h2g_error_string.restype = C.c_char_p
     L.h2g_last_error_detail.restype = C.c_char_p

@@ -158,4 +158,25 @@ __global__ void scatter_batch_kernel(const double* __restrict__ in,
   }
 }
 
+// multi-GPU exchange: copy (src, dst, len) slot ranges between buffers
+struct CopyRange {
+  int64_t src, dst, len;
+};
+
+__global__ void copy_ranges_kernel(const CopyRange* __restrict__ r, int n,
+                                   const double* __restrict__ src, double* __restrict__ dst) {
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const CopyRange c = r[k];
+    for (int64_t i = threadIdx.x; i < c.len; i += blockDim.x) dst[c.dst + i] = src[c.src + i];
+  }
+}
+
+// phi[perm[i] * ld] = phi_tree[i] for tree rows i in [i0, i1) (owned rows)
+__global__ void scatter_rows_kernel(const double* __restrict__ in, const int32_t* __restrict__ perm,
+                                    double* __restrict__ phi, int64_t ld, int64_t i0, int64_t i1) {
+  for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < i1;
+       i += (int64_t)gridDim.x * blockDim.x)
+    phi[(int64_t)perm[i] * ld] = in[i];
+}
+
 }  // namespace h2g

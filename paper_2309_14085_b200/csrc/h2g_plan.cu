@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -60,9 +61,28 @@ struct Phase {
   std::string name;
   int64_t task_begin = 0, task_end = 0;  // into d_tasks
   int64_t alg_bytes = 0;                 // operator + vector bytes (algorithmic)
+  int part = 0;                          // 0: before the shard exchange, 1: after
   int64_t cta_off = 0;                   // streaming engine: CTA ranges at d_cta[cta_off ..]
   int32_t n_cta = 0;
   int32_t split = 0;                     // 1: all warps per chunk (narrow phase)
+};
+
+// Multi-GPU ownership: subtrees at level `level` are split into
+// nranks contiguous Morton ranges; clusters at levels >= level belong to the
+// rank owning their subtree, coarser clusters are replicated.
+struct Shard {
+  int rank = 0, nranks = 1;
+  int level = 1;                   // L_s (1 when not sharded)
+  int dim = 2;
+  std::vector<int64_t> sub_lo;     // [nranks + 1] first subtree (index at level L_s) per rank
+  std::vector<int64_t> row_bound;  // [nranks + 1] tree-order row range per rank
+  int owner_of_subtree(int64_t idx) const {
+    int r = 0;
+    while (r + 1 < nranks && idx >= sub_lo[r + 1]) ++r;
+    return r;
+  }
+  // owner of cluster c at level l >= level (in-level index m = c - lo[l])
+  int owner(int64_t m, int l) const { return owner_of_subtree(m >> (dim * (l - level))); }
 };
 
 struct HostSchedule {
@@ -102,6 +122,16 @@ struct h2g_plan {
   int64_t mem_scalars = 0;
   int64_t n_slots = 0;
   int64_t q_tree = 0, phi_tree = 0;
+  // multi-GPU sharding
+  Shard shard;
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> xchg;  // per rank: (slot, len) ranges
+  int64_t send_slots = 0, max_send_slots = 0;
+  CopyRange* d_pack = nullptr;      // this rank's ranges -> send buffer
+  CopyRange* d_unpack = nullptr;    // other ranks' ranges: recv buffer -> arena
+  int n_pack = 0, n_unpack = 0;
+  int64_t row_begin = 0, row_end = 0;
+  cudaGraph_t graph1 = nullptr;      // part 1 (after the exchange) of a sharded plan
+  cudaGraphExec_t graph1_exec = nullptr;
   int64_t ones_off = 0, n_ones = 0;
   cudaStream_t stream = nullptr;
   double* d_blob = nullptr;
@@ -212,13 +242,14 @@ bool in_blob(const h2g_export_desc* d, int64_t off, int64_t rows, int64_t cols) 
   return off >= 0 && rows >= 0 && cols >= 0 && off + rows * cols <= d->blob_len;
 }
 
-int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
+int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const Shard& sh) {
   const int kappa = d->kappa;
   const int dim = d->dim;
   const int64_t nc = d->n_clusters;
   const int64_t* lo = d->level_offset;
   const int64_t* st = d->cl_start;
   const int64_t* en = d->cl_end;
+  const int Ls = sh.level;
   auto nsz = [&](int64_t c) { return en[c] - st[c]; };
   auto parent = [&](int64_t c, int l) { return lo[l - 1] + ((c - lo[l]) >> dim); };
   auto level_of = [&](int64_t c) {
@@ -226,8 +257,10 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
     while (l <= kappa && c >= lo[l + 1]) ++l;
     return l;
   };
+  // cluster c (level l) computed by this rank: replicated below L_s, owned above
+  auto mine = [&](int64_t c, int l) { return l < Ls || sh.owner(c - lo[l], l) == sh.rank; };
 
-  // ---- arena layout (slots) ----
+  // ---- arena layout (slots, identical on every rank) ----
   int64_t slots = 0;
   p->q_tree = slots;
   slots += d->n_points;
@@ -260,22 +293,47 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
     w_off[k] = slots;
     slots += d->blr_rank[k];
   }
-  // split-K partials of BLR stage 1
+  // BLR stage-1 pieces: columns of Y cut on a regular grid and, for factors
+  // whose target is replicated (level < L_s), also at the ranks' row bounds so
+  // every piece has one owner.  Several pieces -> split-K partials.
+  struct Piece { int64_t c0, c1; int owner; };
+  std::vector<std::vector<Piece>> pieces(blr_nnz);
   std::vector<int64_t> part_off(blr_nnz, -1);
-  std::vector<int32_t> n_chunks(blr_nnz, 1);
-  std::vector<int64_t> chunk_cols(blr_nnz, 0);
   int64_t max_parts = 0;
   for (int64_t k = 0; k < blr_nnz; ++k) {
     const int64_t pr = d->blr_rank[k];
-    const int64_t ny = nsz(d->blr_src[k]);
+    const int64_t y = d->blr_src[k];
+    const int64_t ny = nsz(y);
+    const int lx = level_of(blr_x[k]);
     const int64_t cc = std::max<int64_t>(64, kBlrChunkDoubles / std::max<int64_t>(pr, 1));
-    chunk_cols[k] = cc;
-    const int64_t nch = (ny + cc - 1) / cc;
-    if (nch > 1) {
-      n_chunks[k] = (int32_t)nch;
+    std::vector<int64_t> cuts;
+    for (int64_t c = 0; c < ny; c += cc) cuts.push_back(c);
+    const bool coarse = lx < Ls && sh.nranks > 1;
+    if (coarse)
+      for (int r = 1; r < sh.nranks; ++r) {
+        const int64_t b = sh.row_bound[r] - st[y];
+        if (b > 0 && b < ny) cuts.push_back(b);
+      }
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    int owner_x = lx >= Ls ? sh.owner(blr_x[k] - lo[lx], lx) : -1;
+    for (size_t i = 0; i < cuts.size(); ++i) {
+      const int64_t c0 = cuts[i], c1 = i + 1 < cuts.size() ? cuts[i + 1] : ny;
+      int owner = owner_x;
+      if (coarse) {  // owner of the piece's rows
+        owner = 0;
+        while (owner + 1 < sh.nranks && st[y] + c0 >= sh.row_bound[owner + 1]) ++owner;
+      } else if (owner < 0) {
+        owner = sh.rank;  // not sharded: everything is local
+      }
+      pieces[k].push_back({c0, c1, owner});
+    }
+    // replicated-target factors always reduce exchanged partials (even one
+    // piece: its owner is the only rank that computes it)
+    if (pieces[k].size() > 1 || coarse) {
       part_off[k] = slots;
-      slots += nch * pr;
-      max_parts = std::max(max_parts, nch);
+      slots += (int64_t)pieces[k].size() * pr;
+      max_parts = std::max<int64_t>(max_parts, (int64_t)pieces[k].size());
     }
   }
   const int64_t ones_off = slots;  // ones(max_parts): x of the split-K reduce tasks
@@ -284,10 +342,39 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
   p->n_ones = max_parts;
   p->n_slots = slots;
 
-  // ---- up_leaf: P2M of every channel + BLR stage 1 (V^T q) ----
+  // ---- exchange layout: slots each rank produces that other ranks read ----
+  // (v of its clusters at levels >= L_s, partials of its replicated-target
+  // BLR pieces); identical computation on every rank
+  p->xchg.assign(sh.nranks, {});
+  if (sh.nranks > 1) {
+    for (int r = 0; r < sh.nranks; ++r) {
+      auto& rr = p->xchg[r];
+      for (int ch = 0; ch < d->n_channels; ++ch) {
+        const h2g_channel_desc& c = d->channels[ch];
+        for (int l = Ls; l <= kappa; ++l) {
+          const int64_t shift = (int64_t)dim * (l - Ls);
+          const int64_t c0 = lo[l] + (sh.sub_lo[r] << shift);
+          const int64_t c1 = lo[l] + (sh.sub_lo[r + 1] << shift);  // exclusive
+          if (c1 <= c0) continue;
+          const int64_t a = v_off[ch][c0], b = v_off[ch][c1 - 1] + c.r_out[c1 - 1];
+          if (b > a) rr.push_back({a, b - a});
+        }
+      }
+      for (int64_t k = 0; k < blr_nnz; ++k) {
+        if (part_off[k] < 0 || level_of(blr_x[k]) >= Ls) continue;
+        const int64_t pr = d->blr_rank[k];
+        for (size_t i = 0; i < pieces[k].size(); ++i)
+          if (pieces[k][i].owner == r) rr.push_back({part_off[k] + (int64_t)i * pr, pr});
+      }
+    }
+  }
+
+  // ================= part 0: before the exchange =================
+  // ---- up_leaf: P2M of every channel ----
   begin_phase(s, PH_GEMV, "up_leaf");
   int64_t bytes = 0;
   for (int64_t x = lo[kappa]; x < lo[kappa + 1]; ++x) {
+    if (!mine(x, kappa)) continue;
     for (int ch = 0; ch < d->n_channels; ++ch) {
       const h2g_channel_desc& c = d->channels[ch];
       if (c.p2m_off[x] < 0 || c.r_out[x] == 0) continue;
@@ -300,7 +387,7 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
   s.phases.back().alg_bytes = bytes;
   end_phase(s);
 
-  // ---- blr_vq: BLR stage 1, w_XY = V_XY^T q_Y (split-K partials for long Y) ----
+  // ---- blr_vq: BLR stage 1, w_XY = V_XY^T q_Y (pieces -> split-K partials) ----
   begin_phase(s, PH_GEMV, "blr_vq");
   bytes = 0;
   for (int64_t k = 0; k < blr_nnz; ++k) {
@@ -310,45 +397,42 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
     if (pr <= 0) return fail(H2G_ERR_BAD_EXPORT, "BLR factor of rank 0 exported");
     if (!in_blob(d, d->blr_v_off[k], ny, pr) || !in_blob(d, d->blr_u_off[k], nsz(blr_x[k]), pr))
       return fail(H2G_ERR_BAD_EXPORT, "BLR factor out of blob");
-    if (n_chunks[k] == 1) {
-      add_term(s, d->blr_v_off[k], p->q_tree + st[y], pr, ny);
-      emit_task(s, w_off[k], pr, bytes);
-    } else {
-      const int64_t cc = chunk_cols[k];
-      for (int64_t ci = 0; ci < n_chunks[k]; ++ci) {
-        const int64_t c0 = ci * cc;
-        const int64_t ncols = std::min(cc, ny - c0);
-        add_term(s, d->blr_v_off[k] + c0 * pr, p->q_tree + st[y] + c0, pr, ncols);
-        emit_task(s, part_off[k] + ci * pr, pr, bytes);
-      }
+    for (size_t i = 0; i < pieces[k].size(); ++i) {
+      const Piece& pc = pieces[k][i];
+      if (pc.owner != sh.rank) continue;
+      add_term(s, d->blr_v_off[k] + pc.c0 * pr, p->q_tree + st[y] + pc.c0, pr, pc.c1 - pc.c0);
+      emit_task(s, part_off[k] >= 0 ? part_off[k] + (int64_t)i * pr : w_off[k], pr, bytes);
     }
   }
   s.phases.back().alg_bytes = bytes;
   end_phase(s);
-  // split-K reduce tasks w = [partial_0 .. partial_C-1] * ones, emitted into
-  // the next launched phase (they only need blr_vq to have finished)
+  // split-K reduce tasks w = [partial_0 .. partial_C-1] * ones for the factors
+  // this rank's leaves need; they go into the first phase after the exchange
   auto emit_blr_reduce = [&]() {
     int64_t scratch = 0;
     for (int64_t k = 0; k < blr_nnz; ++k) {
-      if (n_chunks[k] == 1) continue;
-      add_term(s, part_off[k], ones_off, d->blr_rank[k], n_chunks[k], /*a_space=*/1);
+      if (part_off[k] < 0) continue;
+      const int lx = level_of(blr_x[k]);
+      if (!mine(blr_x[k], lx)) continue;
+      add_term(s, part_off[k], ones_off, d->blr_rank[k], (int64_t)pieces[k].size(), /*a_space=*/1);
       emit_task(s, w_off[k], d->blr_rank[k], scratch);
     }
   };
   bool reduce_pending = blr_nnz > 0;
 
-  // ---- upward: M2M levels kappa-1 .. 1 ----
+  // ---- upward: M2M levels kappa-1 .. 1 (owned above L_s, then the exchange) ----
   for (int l = kappa - 1; l >= 1; --l) {
     begin_phase(s, PH_GEMV, "m2m_l" + std::to_string(l));
+    s.phases.back().part = l < Ls ? 1 : 0;
     bytes = 0;
-    if (reduce_pending) {
+    if (reduce_pending && l < Ls) {
       emit_blr_reduce();
       reduce_pending = false;
     }
     for (int ch = 0; ch < d->n_channels; ++ch) {
       const h2g_channel_desc& c = d->channels[ch];
       for (int64_t x = lo[l]; x < lo[l + 1]; ++x) {
-        if (c.r_out[x] == 0) continue;
+        if (c.r_out[x] == 0 || !mine(x, l)) continue;
         const int64_t c0 = lo[l + 1] + ((x - lo[l]) << dim);
         for (int64_t cc = c0; cc < c0 + (1 << dim); ++cc) {
           if (c.m2m_off[cc] < 0 || c.r_out[cc] == 0) continue;
@@ -363,11 +447,13 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
     end_phase(s);
   }
 
+  // ================= part 1: after the exchange =================
   // ---- downward: M2L (+ fused L2L) levels 1 .. kappa ----
   for (int l = 1; l <= kappa; ++l) {
     begin_phase(s, PH_GEMV, "down_l" + std::to_string(l));
+    s.phases.back().part = 1;
     bytes = 0;
-    if (reduce_pending) {  // kappa == 1: no m2m phase
+    if (reduce_pending) {  // no replicated m2m phase (L_s == 1)
       emit_blr_reduce();
       reduce_pending = false;
     }
@@ -375,7 +461,7 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
       const h2g_channel_desc& c = d->channels[ch];
       for (int64_t x = lo[l]; x < lo[l + 1]; ++x) {
         const int64_t ri = c.r_in[x];
-        if (ri == 0) continue;
+        if (ri == 0 || !mine(x, l)) continue;
         for (int64_t k = c.m2l_rowptr[x]; k < c.m2l_rowptr[x + 1]; ++k) {
           const int64_t y = c.m2l_src[k];
           if (y < 0 || y >= nc || level_of(y) != l)
@@ -402,10 +488,11 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
 
   // ---- leaf: L2P + BLR stage 2 + near -> phi_tree ----
   begin_phase(s, PH_GEMV, "leaf");
+  s.phases.back().part = 1;
   bytes = 0;
   for (int64_t x = lo[kappa]; x < lo[kappa + 1]; ++x) {
     const int64_t nx = nsz(x);
-    if (nx == 0) continue;
+    if (nx == 0 || !mine(x, kappa)) continue;
     for (int ch = 0; ch < d->n_channels; ++ch) {
       const h2g_channel_desc& c = d->channels[ch];
       if (c.l2p_off[x] < 0 || c.r_in[x] == 0) continue;
@@ -430,10 +517,8 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s) {
     }
     emit_task(s, p->phi_tree + st[x], nx, bytes);
   }
-  // BLR stage-2 bytes are counted per leaf above; stage-1 in up_leaf.
   s.phases.back().alg_bytes = bytes;
   end_phase(s);
-  (void)level_of;
   return H2G_OK;
 }
 
@@ -696,6 +781,10 @@ void free_plan(h2g_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
   if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
+  if (p->graph1_exec) cudaGraphExecDestroy(p->graph1_exec);
+  if (p->graph1) cudaGraphDestroy(p->graph1);
+  cudaFree(p->d_pack);
+  cudaFree(p->d_unpack);
   if (p->graph) cudaGraphDestroy(p->graph);
   cudaFree(p->d_blob);
   cudaFree(p->d_arena);
@@ -715,9 +804,70 @@ void free_plan(h2g_plan* p) {
   delete p;
 }
 
-int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
+// Shard ownership for (rank, nranks): L_s = the first level with >= 4
+// subtrees per rank (capped at kappa); rank r owns the Morton range
+// [r*S/R, (r+1)*S/R) of the S = 2^(d*L_s) subtrees.
+Shard make_shard(const h2g_export_desc* d, int rank, int nranks) {
+  Shard sh;
+  sh.rank = rank;
+  sh.nranks = nranks;
+  sh.dim = d->dim;
+  sh.level = 1;
+  if (nranks > 1)
+    while (sh.level < d->kappa && (1LL << (d->dim * sh.level)) < 4LL * nranks) ++sh.level;
+  const int64_t S = 1LL << (d->dim * sh.level);
+  sh.sub_lo.resize(nranks + 1);
+  sh.row_bound.resize(nranks + 1);
+  for (int r = 0; r <= nranks; ++r) {
+    sh.sub_lo[r] = (int64_t)r * S / nranks;
+    sh.row_bound[r] = sh.sub_lo[r] >= S ? d->n_points
+                                        : d->cl_start[d->level_offset[sh.level] + sh.sub_lo[r]];
+  }
+  return sh;
+}
+
+// A sharded rank uploads only the operator blocks its tasks read: referenced
+// blob intervals are merged, packed into a local blob and the terms remapped.
+void compact_blob(const h2g_export_desc* d, HostSchedule& s, std::vector<double>& local) {
+  std::vector<std::pair<int64_t, int64_t>> iv;  // [begin, end) in global doubles
+  for (const Task& t : s.tasks)
+    for (int32_t k = t.t_begin; k < t.t_end; ++k) {
+      const Term& tm = s.terms[k];
+      if (tm.a_space != 0 || tm.ncols <= 0) continue;
+      iv.push_back({tm.a_off, tm.a_off + (int64_t)(tm.ncols - 1) * tm.lda + t.m});
+    }
+  std::sort(iv.begin(), iv.end());
+  std::vector<std::pair<int64_t, int64_t>> merged;
+  for (auto& x : iv) {
+    if (!merged.empty() && x.first <= merged.back().second)
+      merged.back().second = std::max(merged.back().second, x.second);
+    else
+      merged.push_back(x);
+  }
+  std::vector<int64_t> base(merged.size());
+  int64_t len = 0;
+  for (size_t i = 0; i < merged.size(); ++i) {
+    base[i] = len;
+    len += merged[i].second - merged[i].first;
+  }
+  local.resize((size_t)len + 16, 0.0);
+  for (size_t i = 0; i < merged.size(); ++i)
+    memcpy(local.data() + base[i], d->blob + merged[i].first,
+           sizeof(double) * (merged[i].second - merged[i].first));
+  for (Term& tm : s.terms) {
+    if (tm.a_space != 0 || tm.ncols <= 0) continue;
+    size_t i = std::upper_bound(merged.begin(), merged.end(), std::make_pair(tm.a_off, INT64_MAX)) -
+               merged.begin() - 1;
+    tm.a_off = base[i] + (tm.a_off - merged[i].first);
+  }
+}
+
+int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank = 0,
+                int nranks = 1) {
   int rc = validate(d);
   if (rc) return rc;
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(H2G_ERR_INVALID_ARG, "bad rank / nranks");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(H2G_ERR_NO_DEVICE, "no CUDA device visible");
@@ -733,11 +883,16 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
   p->N = d->n_points;
   p->mem_scalars = d->mem_scalars;
   HostSchedule s;
-  rc = build_schedule(d, p, s);
+  p->shard = make_shard(d, rank, nranks);
+  rc = build_schedule(d, p, s, p->shard);
   if (rc) {
     delete p;
     return rc;
   }
+  p->row_begin = p->shard.row_bound[rank];
+  p->row_end = p->shard.row_bound[rank + 1];
+  std::vector<double> local_blob;
+  if (nranks > 1) compact_blob(d, s, local_blob);
   {
     const char* e = getenv("H2G_ENGINE");
     if (e && std::string(e) == "ldg") p->engine = 0;
@@ -777,9 +932,43 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
   };
   rc = [&]() -> int {
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-    p->blob_len = d->blob_len;
     int r;
-    if ((r = upload((void**)&p->d_blob, d->blob, sizeof(double) * d->blob_len))) return r;
+    if (nranks > 1) {
+      p->blob_len = (int64_t)local_blob.size();
+      if ((r = upload((void**)&p->d_blob, local_blob.data(), sizeof(double) * local_blob.size())))
+        return r;
+      std::vector<double>().swap(local_blob);
+    } else {
+      p->blob_len = d->blob_len;
+      if ((r = upload((void**)&p->d_blob, d->blob, sizeof(double) * d->blob_len))) return r;
+    }
+    if (nranks > 1) {  // exchange copy lists
+      int64_t mx = 0;
+      for (int q = 0; q < nranks; ++q) {
+        int64_t tot = 0;
+        for (auto& rg : p->xchg[q]) tot += rg.second;
+        mx = std::max(mx, tot);
+      }
+      p->max_send_slots = mx;
+      std::vector<CopyRange> pack, unpack;
+      for (int q = 0; q < nranks; ++q) {
+        int64_t pos = 0;
+        for (auto& rg : p->xchg[q]) {
+          if (q == rank) {
+            pack.push_back({rg.first, pos, rg.second});
+          } else {
+            unpack.push_back({(int64_t)q * mx + pos, rg.first, rg.second});
+          }
+          pos += rg.second;
+        }
+        if (q == rank) p->send_slots = pos;
+      }
+      p->n_pack = (int)pack.size();
+      p->n_unpack = (int)unpack.size();
+      if ((r = upload((void**)&p->d_pack, pack.data(), sizeof(CopyRange) * pack.size()))) return r;
+      if ((r = upload((void**)&p->d_unpack, unpack.data(), sizeof(CopyRange) * unpack.size())))
+        return r;
+    }
     if ((r = upload((void**)&p->d_perm, perm32.data(), sizeof(int32_t) * p->N))) return r;
     if ((r = upload((void**)&p->d_tasks, s.tasks.data(), sizeof(Task) * s.tasks.size()))) return r;
     if ((r = upload((void**)&p->d_terms, s.terms.data(), sizeof(Term) * s.terms.size()))) return r;
@@ -807,19 +996,26 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out) {
                          sizeof(Term) * s.terms.size() +
                          sizeof(ChunkRec) * chunks.size() + sizeof(int64_t) * cta.size() +
                          sizeof(int32_t) * p->N;
-    // capture the fixed middle phases into one CUDA graph
-    CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-    for (const Phase& ph : p->phases) {
-      int lr = launch_phase(p, ph, p->stream);
-      if (lr) {
-        cudaGraph_t g;
-        cudaStreamEndCapture(p->stream, &g);
-        if (g) cudaGraphDestroy(g);
-        return lr;
+    // capture the fixed middle phases into CUDA graphs: one for an unsharded
+    // plan; part 0 / part 1 (around the exchange) for a sharded one
+    for (int part = 0; part < 2; ++part) {
+      if (part == 1 && nranks == 1) break;
+      CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+      for (const Phase& ph : p->phases) {
+        if (nranks > 1 && ph.part != part) continue;
+        int lr = launch_phase(p, ph, p->stream);
+        if (lr) {
+          cudaGraph_t g;
+          cudaStreamEndCapture(p->stream, &g);
+          if (g) cudaGraphDestroy(g);
+          return lr;
+        }
       }
+      cudaGraph_t* gp = part == 0 ? &p->graph : &p->graph1;
+      cudaGraphExec_t* ge = part == 0 ? &p->graph_exec : &p->graph1_exec;
+      CUDA_TRY(cudaStreamEndCapture(p->stream, gp));
+      CUDA_TRY(cudaGraphInstantiate(ge, *gp, 0));
     }
-    CUDA_TRY(cudaStreamEndCapture(p->stream, &p->graph));
-    CUDA_TRY(cudaGraphInstantiate(&p->graph_exec, p->graph, 0));
     CUDA_TRY(cudaStreamSynchronize(p->stream));
     return H2G_OK;
   }();
@@ -875,6 +1071,8 @@ int matvec_impl(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nr
   if (rc) return rc;
   if (!q || !phi) return fail(H2G_ERR_INVALID_ARG, "null vector");
   CUDA_TRY(cudaSetDevice(p->device));
+  if (p->shard.nranks > 1)
+    return fail(H2G_ERR_INVALID_ARG, "sharded plan: use h2g_matvec_begin / exchange / end");
   if (nrhs > 1 && p->engine == 1 && p->use_batched) {
     rc = ensure_batched(p);
     if (rc) return rc;
@@ -927,6 +1125,77 @@ int h2g_plan_create(const h2g_export_desc* desc, int device, h2g_plan** out) {
   if (!out) return fail(H2G_ERR_INVALID_ARG, "null out");
   *out = nullptr;
   return create_impl(desc, device, out);
+}
+
+int h2g_plan_create_sharded(const h2g_export_desc* desc, int device, int rank, int nranks,
+                            h2g_plan** out) {
+  if (!out) return fail(H2G_ERR_INVALID_ARG, "null out");
+  *out = nullptr;
+  return create_impl(desc, device, out, rank, nranks);
+}
+
+int h2g_shard_get_info(const h2g_plan* p, h2g_shard_info* o) {
+  if (!p || !o) return fail(H2G_ERR_INVALID_ARG, "null argument");
+  o->rank = p->shard.rank;
+  o->nranks = p->shard.nranks;
+  o->level = p->shard.level;
+  o->row_begin = p->row_begin;
+  o->row_end = p->row_end;
+  o->send_slots = p->send_slots;
+  o->max_send_slots = p->max_send_slots;
+  o->blob_bytes = 8 * p->blob_len;
+  return H2G_OK;
+}
+
+int h2g_matvec_begin(h2g_plan* p, const double* q_dev, int64_t n, void* stream) {
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  if (n != p->N) return fail(H2G_ERR_LENGTH_MISMATCH, "vector length mismatch");
+  if (!q_dev) return fail(H2G_ERR_INVALID_ARG, "null vector");
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  gather_perm_kernel<<<grid_for(n), 256, 0, s>>>(q_dev, 1, p->d_perm, p->d_arena + p->q_tree, n);
+  CUDA_TRY(cudaGetLastError());
+  if (p->shard.nranks == 1) return run_middle(p, s);  // unsharded: everything here
+  CUDA_TRY(cudaGraphLaunch(p->graph_exec, s));
+  return H2G_OK;
+}
+
+int h2g_shard_pack(h2g_plan* p, double* send_dev, void* stream) {
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  if (p->n_pack == 0) return H2G_OK;
+  if (!send_dev) return fail(H2G_ERR_INVALID_ARG, "null buffer");
+  CUDA_TRY(cudaSetDevice(p->device));
+  copy_ranges_kernel<<<std::min(p->n_pack, 1024), 256, 0, (cudaStream_t)stream>>>(
+      p->d_pack, p->n_pack, p->d_arena, send_dev);
+  CUDA_TRY(cudaGetLastError());
+  return H2G_OK;
+}
+
+int h2g_shard_unpack(h2g_plan* p, const double* recv_dev, void* stream) {
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  if (p->n_unpack == 0) return H2G_OK;
+  if (!recv_dev) return fail(H2G_ERR_INVALID_ARG, "null buffer");
+  CUDA_TRY(cudaSetDevice(p->device));
+  copy_ranges_kernel<<<std::min(p->n_unpack, 1024), 256, 0, (cudaStream_t)stream>>>(
+      p->d_unpack, p->n_unpack, recv_dev, p->d_arena);
+  CUDA_TRY(cudaGetLastError());
+  return H2G_OK;
+}
+
+int h2g_matvec_end(h2g_plan* p, double* phi_dev, int64_t n, void* stream) {
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  if (n != p->N) return fail(H2G_ERR_LENGTH_MISMATCH, "vector length mismatch");
+  if (!phi_dev) return fail(H2G_ERR_INVALID_ARG, "null vector");
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->shard.nranks > 1) CUDA_TRY(cudaGraphLaunch(p->graph1_exec, s));
+  const int64_t rows = p->row_end - p->row_begin;
+  if (rows > 0) {
+    scatter_rows_kernel<<<grid_for(rows), 256, 0, s>>>(p->d_arena + p->phi_tree, p->d_perm,
+                                                       phi_dev, 1, p->row_begin, p->row_end);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return H2G_OK;
 }
 
 int h2g_plan_destroy(h2g_plan* plan) {
@@ -991,13 +1260,105 @@ int h2g_matvec_host(h2g_plan* p, const double* q_host, double* phi_host, int64_t
   return rc;
 }
 
+// ---- host-only schedule view (emulation / tests) ----
+}  // extern "C"
+
+struct h2g_sched {
+  std::map<std::string, std::vector<int64_t>> i64;
+  std::vector<double> blob;
+};
+
+extern "C" {
+
+int h2g_schedule_build(const h2g_export_desc* desc, int rank, int nranks, h2g_sched** out) {
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(H2G_ERR_INVALID_ARG, "bad argument");
+  h2g_plan tmp;
+  HostSchedule s;
+  tmp.shard = make_shard(desc, rank, nranks);
+  rc = build_schedule(desc, &tmp, s, tmp.shard);
+  if (rc) return rc;
+  h2g_sched* o = new h2g_sched();
+  if (nranks > 1) compact_blob(desc, s, o->blob);
+  auto& T = o->i64["tasks"];
+  for (const Task& t : s.tasks) {
+    T.push_back(t.y_off);
+    T.push_back(t.m);
+    T.push_back(t.t_begin);
+    T.push_back(t.t_end);
+  }
+  auto& M = o->i64["terms"];
+  for (const Term& t : s.terms) {
+    M.push_back(t.a_off);
+    M.push_back(t.x_off);
+    M.push_back(t.lda);
+    M.push_back(t.ncols);
+    M.push_back(t.a_space);
+  }
+  auto& P = o->i64["phases"];
+  for (const Phase& ph : s.phases) {
+    P.push_back(ph.task_begin);
+    P.push_back(ph.task_end);
+    P.push_back(ph.part);
+    P.push_back(ph.alg_bytes);
+  }
+  int64_t mx = 0;
+  for (auto& v : tmp.xchg) {
+    int64_t t = 0;
+    for (auto& rg : v) t += rg.second;
+    mx = std::max(mx, t);
+  }
+  auto& PK = o->i64["pack"];
+  auto& UP = o->i64["unpack"];
+  int64_t send = 0;
+  for (int q = 0; q < (int)tmp.xchg.size(); ++q) {
+    int64_t pos = 0;
+    for (auto& rg : tmp.xchg[q]) {
+      if (q == rank) {
+        PK.insert(PK.end(), {rg.first, pos, rg.second});
+      } else {
+        UP.insert(UP.end(), {(int64_t)q * mx + pos, rg.first, rg.second});
+      }
+      pos += rg.second;
+    }
+    if (q == rank) send = pos;
+  }
+  o->i64["meta"] = {tmp.n_slots, tmp.q_tree, tmp.phi_tree, tmp.ones_off, tmp.n_ones,
+                    tmp.shard.row_bound[rank], tmp.shard.row_bound[rank + 1], send, mx,
+                    tmp.shard.level};
+  *out = o;
+  return H2G_OK;
+}
+
+int h2g_schedule_get(const h2g_sched* sc, const char* name, const void** ptr, int64_t* len,
+                     int32_t* is_f64) {
+  if (!sc || !name || !ptr || !len || !is_f64) return fail(H2G_ERR_INVALID_ARG, "bad argument");
+  const std::string n(name);
+  if (n == "blob") {
+    *ptr = sc->blob.data();
+    *len = (int64_t)sc->blob.size();
+    *is_f64 = 1;
+    return H2G_OK;
+  }
+  auto it = sc->i64.find(n);
+  if (it == sc->i64.end()) return fail(H2G_ERR_INVALID_ARG, "no such array");
+  *ptr = it->second.data();
+  *len = (int64_t)it->second.size();
+  *is_f64 = 0;
+  return H2G_OK;
+}
+
+void h2g_schedule_free(h2g_sched* sc) { delete sc; }
+
 int h2g_schedule_info(const h2g_export_desc* desc, int n_sm, char* buf, int64_t buflen) {
   int rc = validate(desc);
   if (rc) return rc;
   if (!buf || buflen <= 0 || n_sm <= 0) return fail(H2G_ERR_INVALID_ARG, "bad buffer / n_sm");
   h2g_plan tmp;
   HostSchedule s;
-  rc = build_schedule(desc, &tmp, s);
+  rc = build_schedule(desc, &tmp, s, make_shard(desc, 0, 1));
   if (rc) return rc;
   std::vector<HostChunk> chunks;
   std::vector<int64_t> cta;

@@ -1,0 +1,194 @@
+"""Multi-GPU matvec: subtree-sharded plans + one all-gather per matvec.
+
+One process per GPU (``torch.distributed``, NCCL).  Rank r of R builds a
+plan restricted to its subtrees (``h2g_plan_create_sharded``, include/h2g.h):
+the Morton range [r*S/R, (r+1)*S/R) of the S subtrees at level L_s, the
+replicated coarse levels, and the BLR V^T q pieces over its own rows.  q is
+replicated.  A matvec is
+
+    h2g_matvec_begin(q)        P2M, BLR pieces, M2M of the owned subtrees
+    h2g_shard_pack(send)       owned multipole coefficients v (levels >= L_s)
+                               + split-K partials of replicated BLR targets
+    all_gather(send -> recv)   NCCL, max_send_slots doubles per rank
+    h2g_shard_unpack(recv)
+    h2g_matvec_end(phi)        coarse M2M, M2L/L2L, L2P + BLR U + near field:
+                               phi rows [row_begin, row_end) of tree order
+
+No reduction of phi is ever needed (rows are owned); ``gather_full=True``
+combines the ranks' rows with one all-reduce (disjoint rows, exact).
+
+``schedule_view`` / ``emulate_matvec`` expose the same per-rank schedule to
+numpy so the sharding logic is tested on CPU with gloo (tests/test_sharded.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .gpu_rep import _desc_from_packed
+from .packed import PackedOperator
+
+
+class ShardedGpuHierRep:
+    def __init__(self, op: PackedOperator, rank: int, nranks: int, device: int = 0,
+                 group=None, lib=None):
+        L = lib or _lib.load()
+        op.validate()
+        desc, keep = _desc_from_packed(op)
+        plan = C.c_void_p()
+        _lib.check(L.h2g_plan_create_sharded(C.byref(desc), int(device), int(rank), int(nranks),
+                                             C.byref(plan)), "h2g_plan_create_sharded", L=L)
+        del keep
+        self._L, self._plan = L, plan
+        self.rank, self.nranks, self.device, self.group = rank, nranks, device, group
+        self.N = op.N
+        self.mem_scalars = op.mem_scalars
+        info = _lib.ShardInfo()
+        _lib.check(L.h2g_shard_get_info(plan, C.byref(info)), L=L)
+        self.info = {f: getattr(info, f) for f, _ in _lib.ShardInfo._fields_}
+        self._send = self._recv = None
+
+    def close(self):
+        if getattr(self, "_plan", None) is not None and self._plan.value:
+            self._L.h2g_plan_destroy(self._plan)
+            self._plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- the three halves (torch CUDA tensors, current stream) ---------------
+    def _buffers(self, torch):
+        if self._send is None:
+            mx = max(1, self.info["max_send_slots"])
+            dev = f"cuda:{self.device}"
+            self._send = torch.zeros(mx, dtype=torch.float64, device=dev)
+            self._recv = torch.zeros(mx * self.nranks, dtype=torch.float64, device=dev)
+        return self._send, self._recv
+
+    def begin(self, q, stream):
+        _lib.check(self._L.h2g_matvec_begin(self._plan, C.c_void_p(q.data_ptr()), self.N,
+                                            C.c_void_p(stream)), "h2g_matvec_begin", L=self._L)
+
+    def pack(self, send, stream):
+        _lib.check(self._L.h2g_shard_pack(self._plan, C.c_void_p(send.data_ptr()),
+                                          C.c_void_p(stream)), L=self._L)
+
+    def unpack(self, recv, stream):
+        _lib.check(self._L.h2g_shard_unpack(self._plan, C.c_void_p(recv.data_ptr()),
+                                            C.c_void_p(stream)), L=self._L)
+
+    def end(self, phi, stream):
+        _lib.check(self._L.h2g_matvec_end(self._plan, C.c_void_p(phi.data_ptr()), self.N,
+                                          C.c_void_p(stream)), "h2g_matvec_end", L=self._L)
+
+    def matvec(self, q, gather_full: bool = False):
+        """phi = K~ q on this rank's rows (torch CUDA tensor q, replicated)."""
+        import torch
+        import torch.distributed as dist
+        if q.shape[0] != self.N:
+            raise ValueError("vector length mismatch")
+        q = q.to(torch.float64).contiguous()
+        stream = torch.cuda.current_stream(q.device).cuda_stream
+        phi = torch.zeros_like(q)
+        send, recv = self._buffers(torch)
+        self.begin(q, stream)
+        if self.nranks > 1:
+            self.pack(send, stream)
+            dist.all_gather_into_tensor(recv, send, group=self.group)
+            self.unpack(recv, stream)
+        self.end(phi, stream)
+        if gather_full and self.nranks > 1:
+            dist.all_reduce(phi, group=self.group)  # disjoint rows: exact
+        return phi
+
+
+# ------------------------------------------------------------ CPU emulation
+def schedule_view(op: PackedOperator, rank: int = 0, nranks: int = 1) -> dict:
+    """Rank's host schedule (include/h2g.h h2g_schedule_build) as numpy arrays."""
+    L = _lib.load()
+    desc, keep = _desc_from_packed(op)
+    h = C.c_void_p()
+    _lib.check(L.h2g_schedule_build(C.byref(desc), int(rank), int(nranks), C.byref(h)),
+               "h2g_schedule_build")
+    out = {}
+    try:
+        for name, cols in (("tasks", 4), ("terms", 5), ("phases", 4), ("pack", 3),
+                           ("unpack", 3), ("meta", 1), ("blob", 1)):
+            ptr, n, is_f64 = C.c_void_p(), C.c_int64(), C.c_int32()
+            _lib.check(L.h2g_schedule_get(h, name.encode(), C.byref(ptr), C.byref(n),
+                                          C.byref(is_f64)))
+            dt = np.float64 if is_f64.value else np.int64
+            if n.value:
+                buf = (C.c_char * (n.value * 8)).from_address(ptr.value)
+                a = np.frombuffer(buf, dtype=dt, count=n.value).copy()
+            else:
+                a = np.zeros(0, dt)
+            out[name] = a.reshape(-1, cols) if cols > 1 else a
+    finally:
+        L.h2g_schedule_free(h)
+    del keep
+    m = out["meta"]
+    out.update(n_slots=int(m[0]), q_tree=int(m[1]), phi_tree=int(m[2]), ones_off=int(m[3]),
+               n_ones=int(m[4]), row_begin=int(m[5]), row_end=int(m[6]), send_slots=int(m[7]),
+               max_send_slots=int(m[8]), level=int(m[9]))
+    return out
+
+
+def _run_phases(view, blob, arena, part):
+    tasks, terms = view["tasks"], view["terms"]
+    for tb, te, ph_part, _ in view["phases"]:
+        if ph_part != part:
+            continue
+        for y_off, m, t0, t1 in tasks[tb:te]:
+            acc = np.zeros(m)
+            for a_off, x_off, lda, ncols, a_space in terms[t0:t1]:
+                src = arena if a_space else blob
+                A = np.lib.stride_tricks.as_strided(src[a_off:], shape=(m, ncols),
+                                                    strides=(8, 8 * lda))
+                acc += A @ arena[x_off:x_off + ncols]
+            arena[y_off:y_off + m] = acc
+
+
+def emulate_begin(view, op, q):
+    """Part 0 of a rank's matvec in numpy; returns (arena, send)."""
+    blob = view["blob"] if len(view["blob"]) else op.blob
+    arena = np.zeros(view["n_slots"] + 8)
+    arena[view["ones_off"]:view["ones_off"] + view["n_ones"]] = 1.0
+    arena[view["q_tree"]:view["q_tree"] + op.N] = np.asarray(q, dtype=np.float64)[op.perm]
+    _run_phases(view, blob, arena, 0)
+    send = np.zeros(max(1, view["max_send_slots"]))
+    for src, dst, ln in view["pack"]:
+        send[dst:dst + ln] = arena[src:src + ln]
+    return arena, send
+
+
+def emulate_end(view, op, arena, recv):
+    """Unpack the all-gathered buffer, run part 1; returns phi with this rank's rows."""
+    blob = view["blob"] if len(view["blob"]) else op.blob
+    for src, dst, ln in view["unpack"]:
+        arena[dst:dst + ln] = recv[src:src + ln]
+    _run_phases(view, blob, arena, 1)
+    phi = np.zeros(op.N)
+    rows = np.arange(view["row_begin"], view["row_end"])
+    phi[op.perm[rows]] = arena[view["phi_tree"] + rows]
+    return phi
+
+
+def emulate_matvec(op, q, nranks: int = 1) -> np.ndarray:
+    """All ranks in one process (exchange = concatenation); phi combined."""
+    views = [schedule_view(op, r, nranks) for r in range(nranks)]
+    states = [emulate_begin(v, op, q) for v in views]
+    mx = max(1, views[0]["max_send_slots"])
+    recv = np.zeros(mx * nranks)
+    for r, (_, send) in enumerate(states):
+        recv[r * mx:r * mx + len(send)] = send[:mx]
+    phi = np.zeros(op.N)
+    for v, (arena, _) in zip(views, states):
+        phi += emulate_end(v, op, arena, recv)
+    return phi
