@@ -21,8 +21,10 @@ kernel's achieved algorithmic bytes/s against MEASURED_PEAKS.json.
 (oracle/packed_matvec.py, one core) on a bounded sample.
 
 --impl reference times that CPU port as the reference arm (rank 0 only).
-Multi-GPU (N > 1): interim "replicas" mode -- every rank runs the full
-operator (weak scaling); the subtree-sharded path is DESIGN.md's next row.
+Multi-GPU (N > 1, torchrun, NCCL): the operator is sharded by subtrees
+(ShardedGpuHierRep): each rank holds and streams its share and
+one NCCL all-gather exchanges the multipole coefficients per matvec; the same
+problem on more GPUs (strong scaling), time = max over ranks.
 """
 
 from __future__ import annotations
@@ -52,7 +54,8 @@ CONFIGS = {
     "cfg3": dict(N=1048576, d=3, kernel="lap3d", n_max=64, eps=1e-6,
                  desc="cfg3: 3D N=1048576 uniform [-1,1]^3, 1/r, leaf<=64, eps 1e-6"),
 }
-METRIC = "H2* matvec/s (fp64) on 1 B200, 2D N=1M log r eps 1e-8"
+# BASELINE.json "metric"; config.workload names the configuration measured
+METRIC = "H2* matvec/s and achieved HBM GB/s (fp64, 1/2/4/8 B200) vs ref CPU matvec"
 
 
 def _peaks():
@@ -186,6 +189,45 @@ def bench_variant(op, args, torch, dev, rank, world):
     return res
 
 
+def bench_variant_sharded(op, args, torch, dev, rank, world):
+    """Strong scaling: the operator split over `world` GPUs, one all-gather."""
+    from paper_2309_14085_b200.sharded import ShardedGpuHierRep
+    rep = ShardedGpuHierRep(op, rank, world, device=dev)
+    N = op.N
+    q = np.random.default_rng(43).standard_normal(N)
+    qd = torch.from_numpy(q).to(f"cuda:{dev}")
+    for _ in range(args.warmup):
+        rep.matvec(qd)
+    torch.cuda.synchronize(dev)
+    torch.distributed.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize(dev)
+        ev0.record()
+        for _ in range(args.steps):
+            rep.matvec(qd)
+        ev1.record()
+        torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device=f"cuda:{dev}")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    # e2e: pinned host q -> device, sharded matvec, this rank's rows -> host
+    q_pin = torch.from_numpy(q).pin_memory()
+    phi_pin = torch.empty(N, dtype=torch.float64).pin_memory()
+    torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        qd2 = q_pin.to(f"cuda:{dev}", non_blocking=True)
+        phi_pin.copy_(rep.matvec(qd2), non_blocking=True)
+        torch.cuda.synchronize(dev)
+    e2e = torch.tensor([(time.perf_counter() - t0) / args.steps], device=f"cuda:{dev}")
+    torch.distributed.all_reduce(e2e, op=torch.distributed.ReduceOp.MAX)
+    torch.distributed.barrier()
+    return {"rep": rep, "ms": ms, "prof": [], "clk": clk.summary(), "e2e_s": float(e2e.item()),
+            "q": q, "shard": rep.info}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -247,7 +289,10 @@ def main():
     results = {}
     for v in variants:
         op, tb = build_op(cfg, v, n_threads=n_threads)
-        r = bench_variant(op, args, torch, dev, rank, world)
+        if world > 1:
+            r = bench_variant_sharded(op, args, torch, dev, rank, world)
+        else:
+            r = bench_variant(op, args, torch, dev, rank, world)
         r["op"] = op
         r["build_s"] = tb
         results[v] = r
@@ -257,15 +302,24 @@ def main():
     head = variants[0]
     R = results[head]
     op, rep = R["op"], R["rep"]
-    mvps = 1e3 / R["ms"]
-    value = mvps * world
-    # roofline: streaming GEMV kernel phases (algorithmic bytes / event time)
-    gemv = [p for p in R["prof"] if p["phase"] not in ("gather", "scatter", "blr_reduce")]
-    k_bytes = sum(p["bytes"] for p in gemv)
-    k_ms = sum(p["ms"] for p in gemv)
+    alg_bytes = 8 * op.mem_scalars + 16 * op.N
+    value = 1e3 / R["ms"]  # whole-job matvecs/s (one operator, sharded over `world` GPUs)
     peak, peak_src = _peaks()
-    achieved = k_bytes / (k_ms * 1e-3) / 1e9
-    dom = max(gemv, key=lambda p: p["ms"])
+    if world == 1:
+        # roofline: streaming GEMV kernel phases (algorithmic bytes / event time)
+        gemv = [p for p in R["prof"] if p["phase"] not in ("gather", "scatter", "blr_reduce")]
+        k_bytes = sum(p["bytes"] for p in gemv)
+        k_ms = sum(p["ms"] for p in gemv)
+        achieved = k_bytes / (k_ms * 1e-3) / 1e9
+        dom = max(gemv, key=lambda p: p["ms"])
+        dom = {"name": dom["phase"], "ms": dom["ms"],
+               "GBps": dom["bytes"] / (dom["ms"] * 1e-3) / 1e9}
+        kernel = "stream_gemv_kernel (all GEMV phases)"
+    else:
+        # per-GPU share of the algorithmic bytes over the whole (max-over-ranks) step
+        achieved = alg_bytes / world / (R["ms"] * 1e-3) / 1e9
+        dom = None
+        kernel = "whole sharded matvec per GPU (all phases + NCCL all-gather)"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{head}.json")
     if os.path.exists(tpath):
@@ -276,31 +330,32 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": R["ms"],
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (uniform_points seed 42, q ~ N(0,1) seed 43)",
         "config": {"workload": cfg["desc"], "variant": head, "N": op.N, "kappa": op.kappa,
-                   "mem_scalars": int(op.mem_scalars), "alg_bytes": rep.alg_bytes,
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "mem_scalars": int(op.mem_scalars), "alg_bytes": alg_bytes,
+                   "parallelism": f"subtree-sharded x{world}" if world > 1 else "single",
                    "l2": "operator > L2 (no flush)", "build_s": round(R["build_s"], 2)},
-        "achieved_GBps": rep.alg_bytes / (R["ms"] * 1e-3) / 1e9,
+        "achieved_GBps": alg_bytes / (R["ms"] * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "stream_gemv_kernel (all GEMV phases)",
-                     "dominant_phase": {"name": dom["phase"], "ms": dom["ms"],
-                                        "GBps": dom["bytes"] / (dom["ms"] * 1e-3) / 1e9}},
-        "e2e": {"value": world / R["e2e_s"], "unit": "matvec/s",
+                     "kernel": kernel, "dominant_phase": dom},
+        "e2e": {"value": 1.0 / R["e2e_s"], "unit": "matvec/s",
                 "h2d_bytes_per_step": 8 * op.N, "d2h_bytes_per_step": 8 * op.N},
         "gpu_launches": args.steps * rep.launches_per_matvec(),
         "clocks": R["clk"],
         "phases_us": {p["phase"]: round(p["ms"] * 1e3, 1) for p in R["prof"]},
     }
+    if world > 1:
+        line["shard"] = R["shard"]
     others = {}
     for v in variants[1:]:
         r = results[v]
-        others[v] = {"ms_per_step": r["ms"], "matvec_per_s": 1e3 / r["ms"] * world,
+        others[v] = {"ms_per_step": r["ms"], "matvec_per_s": 1e3 / r["ms"],
                      "mem_scalars": int(r["op"].mem_scalars),
                      "achieved_GBps": (8 * r["op"].mem_scalars + 16 * r["op"].N) / (r["ms"] * 1e-3) / 1e9,
-                     "e2e_matvec_per_s": world / r["e2e_s"], "build_s": round(r["build_s"], 2)}
+                     "e2e_matvec_per_s": 1.0 / r["e2e_s"], "build_s": round(r["build_s"], 2)}
     if others:
         line["variants"] = others
     if rank == 0 and world == 1:

@@ -51,6 +51,10 @@ class ShardedGpuHierRep:
         self.info = {f: getattr(info, f) for f, _ in _lib.ShardInfo._fields_}
         self._send = self._recv = None
 
+    def launches_per_matvec(self) -> int:
+        """gather + phases + scatter (h2g_launches_per_matvec) + pack + unpack."""
+        return int(self._L.h2g_launches_per_matvec(self._plan, 1)) + (2 if self.nranks > 1 else 0)
+
     def close(self):
         if getattr(self, "_plan", None) is not None and self._plan.value:
             self._L.h2g_plan_destroy(self._plan)
