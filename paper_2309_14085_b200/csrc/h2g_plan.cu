@@ -94,7 +94,8 @@ struct HostSchedule {
 };
 
 constexpr int kBlrChunkDoubles = 65536;  // split-K piece of a BLR V^T q product (512 KB)
-constexpr int kRhsBatch = 8;             // right-hand sides per batched pass
+// batched-RHS engines: 8 or 16 right-hand sides per operator pass
+constexpr int kBatchKB[2] = {8, 16};
 
 struct HostChunk {      // streaming chunk before decoding into a ChunkRec
   int64_t a_off;        // offset (doubles) of the first operator entry (blob or arena)
@@ -152,14 +153,17 @@ struct h2g_plan {
   int64_t workspace_bytes = 0;
   // batched-RHS engine (built on first nrhs > 1 call)
   HostSchedule sched;               // host schedule kept for the batched build
-  std::vector<Phase> phases_b;
-  double* d_arena_b = nullptr;      // n_slots x kRhsBatch
-  ChunkRec* d_recs_b = nullptr;
-  int64_t* d_cta_b = nullptr;
-  cudaGraph_t graph_b = nullptr;
-  cudaGraphExec_t graph_b_exec = nullptr;
-  bool batched_ready = false;
+  struct Batched {
+    std::vector<Phase> phases;
+    double* d_arena = nullptr;      // n_slots x KB
+    ChunkRec* d_recs = nullptr;
+    int64_t* d_cta = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool ready = false;
+  } bat[2];                         // KB = kBatchKB[i]
   bool use_batched = true;  // nrhs > 1 through the batched engine (H2G_BATCHED=0: column loop)
+  bool batch_dfma = false;  // H2G_BATCH_ENGINE=dfma: KB = 8 DFMA consumer (diagnostic)
   double* d_hq = nullptr;    // host-call staging (h2g_matvec_host)
   double* d_hphi = nullptr;
   size_t h_cap = 0;
@@ -533,7 +537,7 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
 // null chunks.
 void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
                   std::vector<HostChunk>& chunks, std::vector<Seg>& segs,
-                  std::vector<int64_t>& cta, int kb = 1) {
+                  std::vector<int64_t>& cta, int kb = 1, bool mma = false) {
   for (Phase& ph : phases) {
     if (ph.kind != PH_GEMV) continue;
     const int64_t nt = ph.task_end - ph.task_begin;
@@ -553,8 +557,15 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
         const bool strided = tm.lda != t.m;
         const int64_t ldas = strided ? ((t.m + 1) & ~1) + 2 : t.m;
         int64_t per = std::max<int64_t>(
-            1, std::min<int64_t>(kChunkCols, kChunkA / std::max<int64_t>(ldas, 1)));
+            1, std::min<int64_t>(kChunkCols, mma ? kChunkAMma / (ldas + kb)
+                                                 : kChunkA / std::max<int64_t>(ldas, 1)));
         if (strided) per = std::min<int64_t>(per, kMaxCopies);  // one bulk copy per column
+        if (mma) {  // whole 4-column k-steps, and enough of them per warp for tall tasks
+          const int64_t cap = (kRingMma / 2) / (ldas + kb);
+          if (!strided)
+            per = std::max<int64_t>(per, std::min<int64_t>({kMmaMinCols, cap, kChunkCols}));
+          if (per >= 4) per &= ~int64_t(3);
+        }
         int64_t c0 = 0;
         while (c0 < tm.ncols) {
           const int64_t a_here = tm.a_off + c0 * tm.lda;
@@ -627,7 +638,8 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
     cut_at.push_back(nt);
     // narrow phase (fewer tasks than consumer warps on the GPU): split mode
     // (single RHS only; the batched engine always runs owned tasks)
-    ph.split = (kb == 1 && nt < (int64_t)kConsumers * n_cta) ? 1 : 0;
+    // (the tensor-pipe batched engine shares every chunk among the warps)
+    ph.split = (mma || (kb == 1 && nt < (int64_t)kConsumers * n_cta)) ? 1 : 0;
     // per CTA: tasks -> warps (greedy by cost), interleave queues
     ph.cta_off = (int64_t)cta.size();
     for (size_t g = 0; g + 1 < cut_at.size(); ++g) {
@@ -792,11 +804,13 @@ void free_plan(h2g_plan* p) {
   cudaFree(p->d_tasks);
   cudaFree(p->d_terms);
   cudaFree(p->d_recs);
-  if (p->graph_b_exec) cudaGraphExecDestroy(p->graph_b_exec);
-  if (p->graph_b) cudaGraphDestroy(p->graph_b);
-  cudaFree(p->d_arena_b);
-  cudaFree(p->d_recs_b);
-  cudaFree(p->d_cta_b);
+  for (auto& b : p->bat) {
+    if (b.exec) cudaGraphExecDestroy(b.exec);
+    if (b.graph) cudaGraphDestroy(b.graph);
+    cudaFree(b.d_arena);
+    cudaFree(b.d_recs);
+    cudaFree(b.d_cta);
+  }
   cudaFree(p->d_hq);
   cudaFree(p->d_hphi);
   cudaFree(p->d_cta);
@@ -898,6 +912,8 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     if (e && std::string(e) == "ldg") p->engine = 0;
     const char* b = getenv("H2G_BATCHED");
     if (b && std::string(b) == "0") p->use_batched = false;
+    const char* be = getenv("H2G_BATCH_ENGINE");
+    if (be && std::string(be) == "dfma") p->batch_dfma = true;
     int nsm = 0;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess &&
         nsm > 0)
@@ -977,8 +993,12 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
-    CUDA_TRY(cudaFuncSetAttribute(stream_gemm_kernel<kRhsBatch>,
+    CUDA_TRY(cudaFuncSetAttribute(stream_gemm_kernel<8>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
+    CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<8>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem));
+    CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<16>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem));
     // +8 slots of slack: aligned bulk copies of x may read up to 8 bytes past a slice
     CUDA_TRY(cudaMalloc((void**)&p->d_arena, sizeof(double) * (p->n_slots + 8)));
     CUDA_TRY(cudaMemset(p->d_arena, 0, sizeof(double) * (p->n_slots + 8)));
@@ -1029,40 +1049,57 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
   return H2G_OK;
 }
 
-// Batched-RHS schedule: the same tasks, cut into chunks whose X (ncols x
-// kRhsBatch) also fits the ring, over an arena of kRhsBatch-wide slots.
-int ensure_batched(h2g_plan* p) {
-  if (p->batched_ready) return H2G_OK;
+// Batched-RHS schedule (KB = kBatchKB[which]): the same tasks, cut into
+// chunks whose X (ncols x KB) also fits the ring, over an arena of KB-wide
+// slots; every chunk shared by the consumer warps of the tensor-pipe engine.
+int ensure_batched(h2g_plan* p, int which) {
+  h2g_plan::Batched& b = p->bat[which];
+  if (b.ready) return H2G_OK;
+  const int kb = kBatchKB[which];
+  const bool mma = !p->batch_dfma;
   std::vector<HostChunk> chunks;
   std::vector<int64_t> cta;
   std::vector<Seg> segs;
-  p->phases_b = p->sched.phases;
-  build_chunks(p->sched, p->phases_b, p->n_sm * kCtasPerSm, chunks, segs, cta, kRhsBatch);
-  const size_t slots = (size_t)(p->n_slots + 8) * kRhsBatch;
-  CUDA_TRY(cudaMalloc((void**)&p->d_arena_b, sizeof(double) * slots));
-  CUDA_TRY(cudaMemset(p->d_arena_b, 0, sizeof(double) * slots));
+  b.phases = p->sched.phases;
+  build_chunks(p->sched, b.phases, p->n_sm * (mma ? kMmaCtasPerSm : kCtasPerSm), chunks, segs,
+               cta, kb, mma);
+  const size_t slots = (size_t)(p->n_slots + 8) * kb;
+  CUDA_TRY(cudaMalloc((void**)&b.d_arena, sizeof(double) * slots));
+  CUDA_TRY(cudaMemset(b.d_arena, 0, sizeof(double) * slots));
   if (p->n_ones > 0) {
-    std::vector<double> ones((size_t)p->n_ones * kRhsBatch, 1.0);
-    CUDA_TRY(cudaMemcpy(p->d_arena_b + (size_t)p->ones_off * kRhsBatch, ones.data(),
+    std::vector<double> ones((size_t)p->n_ones * kb, 1.0);
+    CUDA_TRY(cudaMemcpy(b.d_arena + (size_t)p->ones_off * kb, ones.data(),
                         sizeof(double) * ones.size(), cudaMemcpyHostToDevice));
   }
   std::vector<ChunkRec> recs;
-  make_records(chunks, segs, p->d_blob, p->d_arena_b, recs, kRhsBatch);
-  CUDA_TRY(cudaMalloc((void**)&p->d_recs_b, sizeof(ChunkRec) * recs.size()));
-  CUDA_TRY(cudaMemcpy(p->d_recs_b, recs.data(), sizeof(ChunkRec) * recs.size(),
+  make_records(chunks, segs, p->d_blob, b.d_arena, recs, kb);
+  CUDA_TRY(cudaMalloc((void**)&b.d_recs, sizeof(ChunkRec) * recs.size()));
+  CUDA_TRY(cudaMemcpy(b.d_recs, recs.data(), sizeof(ChunkRec) * recs.size(),
                       cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMalloc((void**)&p->d_cta_b, sizeof(int64_t) * cta.size()));
-  CUDA_TRY(cudaMemcpy(p->d_cta_b, cta.data(), sizeof(int64_t) * cta.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc((void**)&b.d_cta, sizeof(int64_t) * cta.size()));
+  CUDA_TRY(cudaMemcpy(b.d_cta, cta.data(), sizeof(int64_t) * cta.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-  for (const Phase& ph : p->phases_b) {
-    stream_gemm_kernel<kRhsBatch><<<ph.n_cta, kStreamThreads, kStreamSmem, p->stream>>>(
-        p->d_recs_b, p->d_cta_b + ph.cta_off, p->d_arena_b);
+  for (const Phase& ph : b.phases) {
+    if (!mma)
+      stream_gemm_kernel<8><<<ph.n_cta, kStreamThreads, kStreamSmem, p->stream>>>(
+          b.d_recs, b.d_cta + ph.cta_off, b.d_arena);
+    else if (kb == 8)
+      stream_mma_kernel<8><<<ph.n_cta, kMmaThreads, kMmaSmem, p->stream>>>(
+          b.d_recs, b.d_cta + ph.cta_off, b.d_arena);
+    else
+      stream_mma_kernel<16><<<ph.n_cta, kMmaThreads, kMmaSmem, p->stream>>>(
+          b.d_recs, b.d_cta + ph.cta_off, b.d_arena);
   }
-  CUDA_TRY(cudaStreamEndCapture(p->stream, &p->graph_b));
-  CUDA_TRY(cudaGraphInstantiate(&p->graph_b_exec, p->graph_b, 0));
+  CUDA_TRY(cudaStreamEndCapture(p->stream, &b.graph));
+  CUDA_TRY(cudaGraphInstantiate(&b.exec, b.graph, 0));
   p->workspace_bytes += sizeof(double) * slots + sizeof(ChunkRec) * recs.size();
-  p->batched_ready = true;
+  b.ready = true;
   return H2G_OK;
+}
+
+// Engine for nrhs right-hand sides: 16-wide passes when more than 8 remain.
+inline int batch_which(const h2g_plan* p, int64_t nrhs) {
+  return (!p->batch_dfma && nrhs > 8) ? 1 : 0;
 }
 
 int matvec_impl(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nrhs, int64_t ld,
@@ -1074,17 +1111,29 @@ int matvec_impl(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nr
   if (p->shard.nranks > 1)
     return fail(H2G_ERR_INVALID_ARG, "sharded plan: use h2g_matvec_begin / exchange / end");
   if (nrhs > 1 && p->engine == 1 && p->use_batched) {
-    rc = ensure_batched(p);
-    if (rc) return rc;
-    for (int64_t c0 = 0; c0 < nrhs; c0 += kRhsBatch) {
-      const int nb = (int)std::min<int64_t>(kRhsBatch, nrhs - c0);
-      gather_batch_kernel<kRhsBatch><<<grid_for(n), 256, 0, s>>>(
-          q, ld, c0, nb, p->d_perm, p->d_arena_b + (size_t)p->q_tree * kRhsBatch, n);
+    for (int64_t c0 = 0; c0 < nrhs;) {
+      const int which = batch_which(p, nrhs - c0);
+      const int kb = kBatchKB[which];
+      rc = ensure_batched(p, which);
+      if (rc) return rc;
+      const h2g_plan::Batched& b = p->bat[which];
+      const int nb = (int)std::min<int64_t>(kb, nrhs - c0);
+      if (kb == 8)
+        gather_batch_kernel<8><<<grid_for(n), 256, 0, s>>>(
+            q, ld, c0, nb, p->d_perm, b.d_arena + (size_t)p->q_tree * kb, n);
+      else
+        gather_batch_kernel<16><<<grid_for(n), 256, 0, s>>>(
+            q, ld, c0, nb, p->d_perm, b.d_arena + (size_t)p->q_tree * kb, n);
       CUDA_TRY(cudaGetLastError());
-      CUDA_TRY(cudaGraphLaunch(p->graph_b_exec, s));
-      scatter_batch_kernel<kRhsBatch><<<grid_for(n), 256, 0, s>>>(
-          p->d_arena_b + (size_t)p->phi_tree * kRhsBatch, p->d_perm, phi, ld, c0, nb, n);
+      CUDA_TRY(cudaGraphLaunch(b.exec, s));
+      if (kb == 8)
+        scatter_batch_kernel<8><<<grid_for(n), 256, 0, s>>>(
+            b.d_arena + (size_t)p->phi_tree * kb, p->d_perm, phi, ld, c0, nb, n);
+      else
+        scatter_batch_kernel<16><<<grid_for(n), 256, 0, s>>>(
+            b.d_arena + (size_t)p->phi_tree * kb, p->d_perm, phi, ld, c0, nb, n);
       CUDA_TRY(cudaGetLastError());
+      c0 += nb;
     }
     return H2G_OK;
   }
@@ -1221,8 +1270,12 @@ int h2g_plan_get_stats(const h2g_plan* p, h2g_plan_stats* o) {
 
 int h2g_launches_per_matvec(const h2g_plan* p, int64_t nrhs) {
   if (!p) return 0;
-  if (nrhs > 1 && p->engine == 1 && p->use_batched)
-    return (int)((p->sched.phases.size() + 2) * ((nrhs + kRhsBatch - 1) / kRhsBatch));
+  if (nrhs > 1 && p->engine == 1 && p->use_batched) {
+    int total = 0;
+    for (int64_t c0 = 0; c0 < nrhs; c0 += kBatchKB[batch_which(p, nrhs - c0)])
+      total += (int)p->sched.phases.size() + 2;
+    return total;
+  }
   return (int)((p->phases.size() + 2) * (nrhs < 1 ? 1 : nrhs));
 }
 

@@ -428,6 +428,320 @@ stream_gemm_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict_
   }
 }
 
+// ------------------------------------------------------------------------
+// Batched-RHS engine on the fp64 tensor pipe (DMMA, mma.sync m8n8k4 f64).
+//
+// Y (m x KB) += A (m x ncols) X (ncols x KB) per chunk: 8-row tiles of A by
+// 4-column k-steps, NT = KB / 8 column tiles of X.  Fragments (PTX ISA
+// m8n8k4 .f64): lane holds A[lane / 4][lane % 4], B[lane % 4][lane / 4] and
+// C[lane / 4][2 (lane % 4) + {0, 1}].  Every chunk is SHARED by the four
+// consumer warps, split 2-D by the task's row count: wr row groups (8-row
+// tiles dealt round-robin) x wk column groups (k-steps dealt round-robin),
+// wr * wk = 4:
+//   m <= 32: 1 x 4,   m <= 64: 2 x 2,   m <= 256: 4 x 1,
+// so a warp holds at most 8 tiles x NT accumulators (32 doubles at KB = 16)
+// and column groups are combined at the task's last chunk in fixed warp order
+// through shared memory.  Garbage rows (>= m) are computed and discarded; the
+// k tail of a chunk is zeroed in both operands.  Deterministic, no atomics.
+#ifndef H2G_MMA_CONSUMERS
+#define H2G_MMA_CONSUMERS 4
+#endif
+#ifndef H2G_MMA_CTAS
+#define H2G_MMA_CTAS 2
+#endif
+#ifndef H2G_MMA_RING
+#define H2G_MMA_RING 11264        // 88 KB data ring per CTA
+#endif
+#ifndef H2G_MMA_CHUNK_A
+#define H2G_MMA_CHUNK_A 3072
+#endif
+constexpr int kMmaConsumers = H2G_MMA_CONSUMERS;   // consumer warps sharing every chunk
+constexpr int kMmaThreads = 32 * (1 + kMmaConsumers);
+constexpr int kMmaCtasPerSm = H2G_MMA_CTAS;
+constexpr int kRingMma = H2G_MMA_RING;
+constexpr int kChunkAMma = H2G_MMA_CHUNK_A;        // operator + X doubles per chunk
+#ifndef H2G_MMA_MIN_COLS
+#define H2G_MMA_MIN_COLS 16
+#endif
+constexpr int kMmaMinCols = H2G_MMA_MIN_COLS;      // columns per chunk at least (tall tasks)
+static_assert(kMmaConsumers == 4 || kMmaConsumers == 8 || kMmaConsumers == 12, "mma consumers");
+// row groups per size class (rt = 8-row tiles: <= 4, <= 8, <= 16, <= 32)
+constexpr int kMmaWr3 = kMmaConsumers;             // widest class: all warps split rows
+constexpr int kMaxTpw = kMmaConsumers == 4 ? 8 : 4; // tiles per warp (accumulator sets)
+constexpr int kRedPerWarp = 4 * 2 * 64;            // partial tiles of one warp (doubles)
+constexpr size_t kMmaSmem = (size_t)kRingMma * 8 + (size_t)kMmaConsumers * kRedPerWarp * 8 +
+                            (size_t)kRecRing * 256 + (size_t)(2 * kSlots + kRecRing) * 8 +
+                            (size_t)kSlots * 4;
+static_assert(kRingMma >= kChunkAMma + 16 * 8 + 64, "mma ring smaller than one chunk");
+static_assert(kMmaSmem <= 227 * 1024, "mma smem");
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int TPW, int NT, int KB>
+__device__ __forceinline__ void mma_load(const double* __restrict__ Ap, int tstride,
+                                         const double* __restrict__ Bp, double (&a)[TPW],
+                                         double (&b)[NT]) {
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) b[nt] = Bp[nt * 8];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i) a[i] = Ap[i * tstride];
+}
+
+template <int TPW, int NT>
+__device__ __forceinline__ void mma_step(const double (&a)[TPW], const double (&b)[NT],
+                                         double (&c)[8][2][2]) {
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) dmma(c[i][nt], a[i], b[nt]);
+}
+
+// One chunk for one warp: tiles i < TPW at rows 8 (w_r + wr i), k-steps
+// w_k, w_k + wk, ...  Ab: lane's A element of (tile 0, k-step 0); Bb: lane's
+// X element of (k-step 0, n-tile 0).
+template <int TPW, int NT, int KB>
+__device__ __forceinline__ void consume_mma(const double* __restrict__ Ab, int ldas, int tstride,
+                                            const double* __restrict__ Bb, int ncols, int kq,
+                                            int w_k, int wk, double (&c)[8][2][2]) {
+  const int full = ncols >> 2;                 // whole k-steps
+  const int n_my = full > w_k ? (full - w_k + wk - 1) / wk : 0;
+  const int adv_a = 4 * ldas * wk, adv_b = 4 * KB * wk;
+  const double* Ap = Ab + 4 * ldas * w_k;
+  const double* Bp = Bb + 4 * KB * w_k;
+#pragma unroll 2
+  for (int t = 0; t < n_my; ++t) {
+    double a[TPW], b[NT];
+    mma_load<TPW, NT, KB>(Ap, tstride, Bp, a, b);
+    mma_step<TPW, NT>(a, b, c);
+    Ap += adv_a;
+    Bp += adv_b;
+  }
+  // k tail (ncols % 4 columns): the column group holding k-step `full`
+  if ((ncols & 3) && (full % wk) == w_k) {
+    const bool ok = 4 * full + kq < ncols;
+    const double* At = Ab + 4 * ldas * full;
+    const double* Bt = Bb + 4 * KB * full;
+    double a[TPW], b[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) b[nt] = ok ? Bt[nt * 8] : 0.0;
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) a[i] = ok ? At[i * tstride] : 0.0;
+    mma_step<TPW, NT>(a, b, c);
+  }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kMmaThreads, kMmaCtasPerSm)
+stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__ cta_begin,
+                  double* arena) {
+  constexpr int NT = KB / 8;
+  static_assert(KB == 8 || KB == 16, "KB");
+  extern __shared__ __align__(128) double smem[];
+  double* ring = smem;
+  double* red = smem + kRingMma;
+  ChunkRec* rring = reinterpret_cast<ChunkRec*>(red + kMmaConsumers * kRedPerWarp);
+  uint64_t* full = reinterpret_cast<uint64_t*>(rring + kRecRing);
+  uint64_t* empty = full + kSlots;
+  uint64_t* recbar = empty + kSlots;
+  int* slot_off = reinterpret_cast<int*>(recbar + kRecRing);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t cb = cta_begin[blockIdx.x];
+  const int n = (int)(cta_begin[blockIdx.x + 1] - cb);
+  const ChunkRec* my = recs + cb;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kMmaConsumers);
+    }
+    for (int r = 0; r < kRecRing; ++r) mbar_init(&recbar[r], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // producer: as stream_gemv_kernel, plus the chunk's X by TMA
+    int oldest = 0, head = 0, tail = 0;
+    if (lane == 0)
+      for (int j = 0; j < kRecAhead && j < n; ++j) {
+        mbar_arrive_expect_tx(&recbar[j], sizeof(ChunkRec));
+        bulk_g2s(&rring[j], my + j, sizeof(ChunkRec), &recbar[j]);
+      }
+    for (int i = 0; i < n; ++i) {
+      const int s = i % kSlots;
+      const int r = i % kRecRing;
+      mbar_wait(&recbar[r], (uint32_t)(i / kRecRing) & 1u);
+      const ChunkRec& h = rring[r];
+      int off = 0;
+      if (lane == 0) {
+        const int need = h.extent;
+        auto release_oldest = [&]() {
+          mbar_wait(&empty[oldest % kSlots], (uint32_t)(oldest / kSlots) & 1u);
+          ++oldest;
+          tail = oldest < i ? slot_off[oldest % kSlots] : head;
+        };
+        while (i - oldest >= kSlots) release_oldest();
+        while (true) {
+          if (oldest == i) {
+            head = tail = 0;
+            off = 0;
+            break;
+          }
+          if (head >= tail) {
+            if (kRingMma - head >= need) { off = head; break; }
+            if (tail > need) { off = 0; break; }
+          } else if (tail - head > need) {
+            off = head;
+            break;
+          }
+          release_oldest();
+        }
+        head = off + need;
+        slot_off[s] = off;
+        const int j = i + kRecAhead;
+        if (j < n) {
+          const int rj = j % kRecRing;
+          mbar_arrive_expect_tx(&recbar[rj], sizeof(ChunkRec));
+          bulk_g2s(&rring[rj], my + j, sizeof(ChunkRec), &recbar[rj]);
+        }
+        mbar_arrive_expect_tx(&full[s], h.bytes_a + h.bytes_x);
+      }
+      off = __shfl_sync(0xffffffffu, off, 0);
+      char* st = reinterpret_cast<char*>(ring + off);
+      if (lane < h.n_copies) {
+        const CopyDesc cd = h.copies[lane];
+        bulk_g2s(st + cd.dst, reinterpret_cast<const void*>(cd.src), cd.bytes, &full[s]);
+      }
+      if (lane < h.n_seg) {
+        const int c0 = h.seg_c0[lane], c1 = h.seg_c0[lane + 1];
+        bulk_g2s(st + 8 * (h.x_base + c0 * KB), reinterpret_cast<const void*>(h.seg_src[lane]),
+                 (uint32_t)(8 * KB * (c1 - c0)), &full[s]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  const int cw = warp - 1;
+  const int kq = lane & 3, rq = lane >> 2;
+  // this warp's (row group, column group) in each size class
+  int cls_wr[4], cls_wk[4], cls_r[4], cls_k[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int wr = k == 3 ? kMmaWr3 : (1 << k);
+    cls_wr[k] = wr;
+    cls_wk[k] = kMmaConsumers / wr;
+    cls_r[k] = cw % wr;
+    cls_k[k] = cw / wr;
+  }
+  double c[8][2][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) c[i][nt][0] = c[i][nt][1] = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const int s = i % kSlots;
+    mbar_wait(&recbar[i % kRecRing], (uint32_t)(i / kRecRing) & 1u);
+    const ChunkRec& h = rring[i % kRecRing];
+    const int m = h.m;
+    const int ncols = h.ncols;
+    const int flags = h.flags;
+    const int ldas = h.ldas;
+    const int a_shift = h.a_shift;
+    const int odd = h.odd_lda;
+    const int x_base = h.x_base;
+    const int64_t y_off = h.y_off;
+    const int rt = (m + 7) >> 3;                     // 8-row tiles
+    const int cls = rt <= 4 ? 0 : (rt <= 8 ? 1 : (rt <= 16 ? 2 : 3));
+    int wr = cls_wr[0], wk = cls_wk[0], w_r = cls_r[0], w_k = cls_k[0];
+#pragma unroll
+    for (int k = 1; k < 4; ++k)
+      if (cls == k) {
+        wr = cls_wr[k];
+        wk = cls_wk[k];
+        w_r = cls_r[k];
+        w_k = cls_k[k];
+      }
+    const int tpw = w_r < rt ? (rt - w_r + wr - 1) / wr : 0;  // this warp's tiles
+    mbar_wait(&full[s], (uint32_t)(i / kSlots) & 1u);
+    if (ncols > 0 && tpw > 0) {
+      const double* sA = ring + slot_off[s];
+      const int lane_shift = odd ? ((a_shift + kq) & 1) : a_shift;
+      const double* Ab = sA + kq * ldas + lane_shift + rq + 8 * w_r;
+      const double* Bb = sA + x_base + kq * KB + rq;
+      const int ts = 8 * wr;
+      switch (tpw) {
+        case 1: consume_mma<1, NT, KB>(Ab, ldas, ts, Bb, ncols, kq, w_k, wk, c); break;
+        case 2: consume_mma<2, NT, KB>(Ab, ldas, ts, Bb, ncols, kq, w_k, wk, c); break;
+        case 3: consume_mma<3, NT, KB>(Ab, ldas, ts, Bb, ncols, kq, w_k, wk, c); break;
+        case 4: consume_mma<4, NT, KB>(Ab, ldas, ts, Bb, ncols, kq, w_k, wk, c); break;
+        default:
+          if constexpr (kMaxTpw > 4) {
+            switch (tpw) {
+              case 5: consume_mma<5, NT, KB>(Ab, ldas, ts, Bb, ncols, kq, w_k, wk, c); break;
+              case 6: consume_mma<6, NT, KB>(Ab, ldas, ts, Bb, ncols, kq, w_k, wk, c); break;
+              case 7: consume_mma<7, NT, KB>(Ab, ldas, ts, Bb, ncols, kq, w_k, wk, c); break;
+              default: consume_mma<8, NT, KB>(Ab, ldas, ts, Bb, ncols, kq, w_k, wk, c); break;
+            }
+          }
+          break;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (flags & kLastOfTask) {
+      double* y = arena + y_off * KB;
+      // classes with wk > 1 have at most 4 tiles per warp
+      if (wk > 1) {  // park partials of column groups 1.. ; group 0 combines them
+        if (w_k > 0) {
+          double* rw = red + cw * kRedPerWarp;
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              *reinterpret_cast<double2*>(rw + (t * 2 + nt) * 64 + 2 * lane) =
+                  make_double2(c[t][nt][0], c[t][nt][1]);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kMmaConsumers * 32) : "memory");
+        if (w_k == 0) {
+          for (int g = 1; g < wk; ++g) {
+            const double* rg = red + (w_r + wr * g) * kRedPerWarp + 2 * lane;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) {
+                const double2 v = *reinterpret_cast<const double2*>(rg + (t * 2 + nt) * 64);
+                c[t][nt][0] += v.x;
+                c[t][nt][1] += v.y;
+              }
+          }
+        }
+      }
+      if (w_k == 0) {
+#pragma unroll
+        for (int t = 0; t < kMaxTpw; ++t) {
+          const int row = 8 * (w_r + wr * t) + rq;
+          if (t < tpw && row < m)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              *reinterpret_cast<double2*>(y + (int64_t)row * KB + nt * 8 + 2 * kq) =
+                  make_double2(c[t][nt][0], c[t][nt][1]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) c[t][nt][0] = c[t][nt][1] = 0.0;
+      if (wk > 1) asm volatile("bar.sync 1, %0;" ::"r"(kMmaConsumers * 32) : "memory");
+    }
+  }
+}
+
 template <bool SPLIT>
 __global__ void __launch_bounds__(kStreamThreads, kCtasPerSm)
 stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__ cta_begin,

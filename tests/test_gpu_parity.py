@@ -116,12 +116,23 @@ def test_native_library_is_loaded(reps):
 
 @pytest.mark.parametrize("name", NAMES)
 def test_batched_rhs_engine(reps, name):
-    """nrhs > 1 runs the batched engine (each operator chunk read once per 8
-    right-hand sides); every column equals the single-RHS matvec and the
-    oracle (the reference's equivalent is a column loop)."""
+    """nrhs > 1 runs the tensor-pipe batched engine (each operator chunk read
+    once per 16 or 8 right-hand sides); every column equals the single-RHS
+    matvec and the oracle (the reference's equivalent is a column loop)."""
     rep, op, z, meta = reps[name]
-    Q = np.random.default_rng(11).standard_normal((op.N, 13))  # 8 + a ragged batch of 5
+    Q = np.random.default_rng(11).standard_normal((op.N, 21))  # 16 + a ragged 8-wide pass of 5
     Phi = rep.matmat(Q)
-    for j in (0, 5, 7, 8, 12):
+    for j in (0, 5, 7, 8, 12, 15, 16, 20):
         assert rel_err(Phi[:, j], rep.matvec(Q[:, j])) <= 1e-13
         assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= TOL
+
+
+def test_batched_engine_edge_widths(reps):
+    """2 and 9 right-hand sides (zero-padded passes) and a zero block."""
+    rep, op, z, meta = reps[NAMES[0]]
+    for k in (2, 9):
+        Q = np.random.default_rng(k).standard_normal((op.N, k))
+        Phi = rep.matmat(Q)
+        for j in range(k):
+            assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= TOL
+    assert np.all(rep.matmat(np.zeros((op.N, 16))) == 0)
