@@ -171,6 +171,31 @@ __global__ void copy_ranges_kernel(const CopyRange* __restrict__ r, int n,
   }
 }
 
+// Split-K reduce for the batched-RHS arena (KB values per slot): y = sum of
+// the task's P partial blocks in piece order (the batched form of the
+// [partials] * ones GEMV task of the single-RHS schedule).
+struct RedTask {
+  int64_t y_off;       // slot of y[0]
+  int64_t part;        // slot of partial 0, row 0 (partial p at part + p * m)
+  int32_t m;
+  int32_t P;
+};
+
+template <int KB>
+__global__ void reduce_partials_kernel(const RedTask* __restrict__ t, int n,
+                                       double* __restrict__ arena) {
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const RedTask r = t[k];
+    const int64_t len = (int64_t)r.m * KB;
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+      const double* src = arena + r.part * KB + i;
+      double acc = 0.0;
+      for (int p = 0; p < r.P; ++p) acc += src[(int64_t)p * len];
+      arena[r.y_off * KB + i] = acc;
+    }
+  }
+}
+
 // phi[perm[i] * ld] = phi_tree[i] for tree rows i in [i0, i1) (owned rows)
 __global__ void scatter_rows_kernel(const double* __restrict__ in, const int32_t* __restrict__ perm,
                                     double* __restrict__ phi, int64_t ld, int64_t i0, int64_t i1) {

@@ -94,6 +94,14 @@ struct HostSchedule {
 };
 
 constexpr int kBlrChunkDoubles = 65536;  // split-K piece of a BLR V^T q product (512 KB)
+// Heavy tasks (one task holding far more than its CTA's share of a phase, e.g.
+// the coarse-level M2L rows of a high-rank kernel) are cut by columns into
+// split-K pieces written to partial slots, combined by a reduce phase that
+// follows (y = [partials] * ones, fixed order).  The split depends only on
+// the schedule, not on the device.
+constexpr int kMaxSplit = 64;
+constexpr int64_t kSplitCtas = 4 * 296;       // pieces per phase: ~4 per persistent CTA
+constexpr int64_t kSplitMinBytes = 1 << 20;   // never cut below 1 MB pieces
 // batched-RHS engines: 8 or 16 right-hand sides per operator pass
 constexpr int kBatchKB[2] = {8, 16};
 
@@ -155,15 +163,17 @@ struct h2g_plan {
   HostSchedule sched;               // host schedule kept for the batched build
   struct Batched {
     std::vector<Phase> phases;
+    std::vector<std::pair<int64_t, int32_t>> red;  // per phase: (offset into d_red, count)
+    RedTask* d_red = nullptr;
     double* d_arena = nullptr;      // n_slots x KB
     ChunkRec* d_recs = nullptr;
     int64_t* d_cta = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     bool ready = false;
+    int launches = 0;               // kernels per pass (graph)
   } bat[2];                         // KB = kBatchKB[i]
   bool use_batched = true;  // nrhs > 1 through the batched engine (H2G_BATCHED=0: column loop)
-  bool batch_dfma = false;  // H2G_BATCH_ENGINE=dfma: KB = 8 DFMA consumer (diagnostic)
   double* d_hq = nullptr;    // host-call staging (h2g_matvec_host)
   double* d_hphi = nullptr;
   size_t h_cap = 0;
@@ -244,6 +254,103 @@ int validate(const h2g_export_desc* d) {
 // Check that an operator [off, off + rows*cols) lies in the blob.
 bool in_blob(const h2g_export_desc* d, int64_t off, int64_t rows, int64_t cols) {
   return off >= 0 && rows >= 0 && cols >= 0 && off + rows * cols <= d->blob_len;
+}
+
+// Cut heavy tasks into split-K pieces (partial slots appended to the arena)
+// and insert a reduce phase after every phase that has some.
+void split_heavy_tasks(HostSchedule& s, int64_t& slots, int64_t ones_off) {
+  std::vector<Task> tasks;
+  std::vector<Term> terms;
+  std::vector<Phase> phases;
+  auto task_bytes = [&](const Task& t) {
+    int64_t c = 0;
+    for (int32_t k = t.t_begin; k < t.t_end; ++k) c += s.terms[k].ncols;
+    return 8 * (int64_t)t.m * c;
+  };
+  auto push_task = [&](int64_t y_off, int32_t m, const std::vector<Term>& tm) {
+    Task t;
+    t.y_off = y_off;
+    t.m = m;
+    t.t_begin = (int32_t)terms.size();
+    for (const Term& u : tm) terms.push_back(u);
+    t.t_end = (int32_t)terms.size();
+    t.pad = 0;
+    tasks.push_back(t);
+  };
+  int64_t min_bytes = kSplitMinBytes;
+  if (const char* e = getenv("H2G_SPLIT_MIN_BYTES")) min_bytes = std::max<int64_t>(64, atoll(e));
+  for (const Phase& ph : s.phases) {
+    int64_t total = 0;
+    for (int64_t i = ph.task_begin; i < ph.task_end; ++i) total += task_bytes(s.tasks[i]);
+    const int64_t thr = std::max<int64_t>(min_bytes, total / kSplitCtas);
+    Phase main = ph;
+    main.task_begin = (int64_t)tasks.size();
+    std::vector<std::pair<Task, std::vector<Term>>> reduces;
+    for (int64_t i = ph.task_begin; i < ph.task_end; ++i) {
+      const Task& t = s.tasks[i];
+      std::vector<Term> tm(s.terms.begin() + t.t_begin, s.terms.begin() + t.t_end);
+      const int64_t tb = task_bytes(t);
+      if (tb <= thr) {
+        push_task(t.y_off, t.m, tm);
+        continue;
+      }
+      int64_t cols = 0;
+      for (const Term& u : tm) cols += u.ncols;
+      const int64_t want = std::min<int64_t>(kMaxSplit, (tb + thr - 1) / thr);
+      const int64_t per = (cols + want - 1) / want;  // columns per piece
+      const int64_t part = slots;
+      int64_t np = 0;
+      std::vector<Term> cur;
+      int64_t in_piece = 0;
+      for (const Term& u : tm) {
+        int64_t c0 = 0;
+        while (c0 < u.ncols) {
+          const int64_t take = std::min<int64_t>(u.ncols - c0, per - in_piece);
+          Term v = u;
+          v.a_off = u.a_off + c0 * u.lda;
+          v.x_off = u.x_off + c0;
+          v.ncols = (int32_t)take;
+          cur.push_back(v);
+          in_piece += take;
+          c0 += take;
+          if (in_piece == per) {
+            push_task(part + np * t.m, t.m, cur);
+            ++np;
+            cur.clear();
+            in_piece = 0;
+          }
+        }
+      }
+      if (!cur.empty()) {
+        push_task(part + np * t.m, t.m, cur);
+        ++np;
+      }
+      slots += np * t.m;
+      Term r;
+      r.a_off = part;
+      r.x_off = ones_off;
+      r.lda = t.m;
+      r.ncols = (int32_t)np;
+      r.a_space = 1;
+      r.pad = 0;
+      Task rt = t;
+      reduces.push_back({rt, std::vector<Term>{r}});
+    }
+    main.task_end = (int64_t)tasks.size();
+    phases.push_back(main);
+    if (!reduces.empty()) {
+      Phase red = ph;
+      red.name = ph.name + "_red";
+      red.alg_bytes = 0;
+      red.task_begin = (int64_t)tasks.size();
+      for (auto& rt : reduces) push_task(rt.first.y_off, rt.first.m, rt.second);
+      red.task_end = (int64_t)tasks.size();
+      phases.push_back(red);
+    }
+  }
+  s.tasks.swap(tasks);
+  s.terms.swap(terms);
+  s.phases.swap(phases);
 }
 
 int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const Shard& sh) {
@@ -340,6 +447,7 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
       max_parts = std::max<int64_t>(max_parts, (int64_t)pieces[k].size());
     }
   }
+  max_parts = std::max<int64_t>(max_parts, kMaxSplit);
   const int64_t ones_off = slots;  // ones(max_parts): x of the split-K reduce tasks
   slots += max_parts;
   p->ones_off = ones_off;
@@ -523,6 +631,7 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
   }
   s.phases.back().alg_bytes = bytes;
   end_phase(s);
+  split_heavy_tasks(s, p->n_slots, ones_off);
   return H2G_OK;
 }
 
@@ -559,7 +668,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
         int64_t per = std::max<int64_t>(
             1, std::min<int64_t>(kChunkCols, mma ? kChunkAMma / (ldas + kb)
                                                  : kChunkA / std::max<int64_t>(ldas, 1)));
-        if (strided) per = std::min<int64_t>(per, kMaxCopies);  // one bulk copy per column
+        if (strided) per = std::min<int64_t>(per, 32);  // one bulk copy per column (producer lane)
         if (mma) {  // whole 4-column k-steps, and enough of them per warp for tall tasks
           const int64_t cap = (kRingMma / 2) / (ldas + kb);
           if (!strided)
@@ -696,6 +805,7 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
     r.n_seg = c.n_seg;
     uint32_t total = 0;
     int nc = 0;
+    int64_t strided_ext = 0;
     const uint64_t blob = c.a_space ? arena : blob0;
     if (c.ncols > 0) {
       const bool strided = c.lda != c.m;
@@ -708,19 +818,20 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
         d.dst = 0;
         d.bytes = round16(8 * (sh + (int64_t)c.m * c.ncols));
         total += d.bytes;
-      } else {
+      } else {  // strided run: one bulk copy per column, issued by the producer lanes
         r.ldas = ((c.m + 1) & ~1) + 2;
         r.a_shift = (int32_t)(c.a_off & 1);
         r.odd_lda = (c.lda & 1) ? 1 : 0;
+        r.flags |= kStridedRun;
+        CopyDesc& d = r.copies[0];
+        d.src = blob + 8 * (uint64_t)c.a_off;
+        d.dst = (uint32_t)c.lda;
+        d.bytes = (uint32_t)c.m;
         for (int k = 0; k < c.ncols; ++k) {
-          const int64_t off = c.a_off + (int64_t)k * c.lda;
-          const int64_t sh = off & 1;
-          CopyDesc& d = r.copies[nc++];
-          d.src = blob + 8 * (uint64_t)(off - sh);
-          d.dst = (uint32_t)(8 * (int64_t)k * r.ldas);
-          d.bytes = round16(8 * (sh + c.m));
-          total += d.bytes;
+          const int64_t sh = (c.a_off + (int64_t)k * c.lda) & 1;
+          total += round16(8 * (sh + c.m));
         }
+        strided_ext = (int64_t)c.ncols * r.ldas;
       }
       int64_t col = 0;
       for (int k = 0; k < c.n_seg; ++k) {
@@ -734,13 +845,13 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
     r.n_copies = nc;
     r.bytes_a = total;
     if (kb > 1) {  // X (ncols x kb) staged after the operator data, 16-byte aligned
-      int64_t ext = 0;
+      int64_t ext = strided_ext;
       for (int k = 0; k < nc; ++k)
         ext = std::max<int64_t>(ext, (r.copies[k].dst + r.copies[k].bytes) / 8);
       r.x_base = (int32_t)((ext + 1) & ~int64_t(1));
       r.bytes_x = (uint32_t)(8 * (int64_t)kb * c.ncols);
     }
-    int64_t ext = 0;
+    int64_t ext = strided_ext;
     for (int k = 0; k < nc; ++k) ext = std::max<int64_t>(ext, (r.copies[k].dst + r.copies[k].bytes) / 8);
     if (kb > 1) ext = std::max<int64_t>(ext, (int64_t)r.x_base + (int64_t)kb * c.ncols);
     r.extent = (int32_t)((ext + 1) & ~int64_t(1));
@@ -810,6 +921,7 @@ void free_plan(h2g_plan* p) {
     cudaFree(b.d_arena);
     cudaFree(b.d_recs);
     cudaFree(b.d_cta);
+    cudaFree(b.d_red);
   }
   cudaFree(p->d_hq);
   cudaFree(p->d_hphi);
@@ -912,8 +1024,6 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     if (e && std::string(e) == "ldg") p->engine = 0;
     const char* b = getenv("H2G_BATCHED");
     if (b && std::string(b) == "0") p->use_batched = false;
-    const char* be = getenv("H2G_BATCH_ENGINE");
-    if (be && std::string(be) == "dfma") p->batch_dfma = true;
     int nsm = 0;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess &&
         nsm > 0)
@@ -993,8 +1103,6 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
-    CUDA_TRY(cudaFuncSetAttribute(stream_gemm_kernel<8>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
     CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<8>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem));
     CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<16>,
@@ -1056,34 +1164,67 @@ int ensure_batched(h2g_plan* p, int which) {
   h2g_plan::Batched& b = p->bat[which];
   if (b.ready) return H2G_OK;
   const int kb = kBatchKB[which];
-  const bool mma = !p->batch_dfma;
+  // Split-K reduce tasks ([partials] * ones) sum per-RHS data, which the
+  // shared-operator GEMM engine cannot express: they run as a reduce kernel
+  // ahead of their phase's GEMM launch (no task of a phase reads another's y).
+  const HostSchedule& s0 = p->sched;
+  HostSchedule sb;
+  std::vector<RedTask> reds;
+  for (const Phase& ph : s0.phases) {
+    Phase q = ph;
+    q.task_begin = (int64_t)sb.tasks.size();
+    const int64_t r0 = (int64_t)reds.size();
+    for (int64_t i = ph.task_begin; i < ph.task_end; ++i) {
+      const Task& t = s0.tasks[i];
+      const Term& t0 = s0.terms[t.t_begin];
+      if (t.t_end - t.t_begin == 1 && t0.a_space == 1 && t0.x_off == p->ones_off) {
+        reds.push_back(RedTask{t.y_off, t0.a_off, t.m, t0.ncols});
+        continue;
+      }
+      Task u = t;
+      u.t_begin = (int32_t)sb.terms.size();
+      for (int32_t k = t.t_begin; k < t.t_end; ++k) sb.terms.push_back(s0.terms[k]);
+      u.t_end = (int32_t)sb.terms.size();
+      sb.tasks.push_back(u);
+    }
+    q.task_end = (int64_t)sb.tasks.size();
+    b.phases.push_back(q);
+    b.red.push_back({r0, (int32_t)((int64_t)reds.size() - r0)});
+  }
   std::vector<HostChunk> chunks;
   std::vector<int64_t> cta;
   std::vector<Seg> segs;
-  b.phases = p->sched.phases;
-  build_chunks(p->sched, b.phases, p->n_sm * (mma ? kMmaCtasPerSm : kCtasPerSm), chunks, segs,
-               cta, kb, mma);
+  build_chunks(sb, b.phases, p->n_sm * kMmaCtasPerSm, chunks, segs, cta, kb, /*mma=*/true);
   const size_t slots = (size_t)(p->n_slots + 8) * kb;
   CUDA_TRY(cudaMalloc((void**)&b.d_arena, sizeof(double) * slots));
   CUDA_TRY(cudaMemset(b.d_arena, 0, sizeof(double) * slots));
-  if (p->n_ones > 0) {
-    std::vector<double> ones((size_t)p->n_ones * kb, 1.0);
-    CUDA_TRY(cudaMemcpy(b.d_arena + (size_t)p->ones_off * kb, ones.data(),
-                        sizeof(double) * ones.size(), cudaMemcpyHostToDevice));
-  }
   std::vector<ChunkRec> recs;
   make_records(chunks, segs, p->d_blob, b.d_arena, recs, kb);
-  CUDA_TRY(cudaMalloc((void**)&b.d_recs, sizeof(ChunkRec) * recs.size()));
-  CUDA_TRY(cudaMemcpy(b.d_recs, recs.data(), sizeof(ChunkRec) * recs.size(),
-                      cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc((void**)&b.d_recs, sizeof(ChunkRec) * std::max<size_t>(1, recs.size())));
+  if (!recs.empty())
+    CUDA_TRY(cudaMemcpy(b.d_recs, recs.data(), sizeof(ChunkRec) * recs.size(),
+                        cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMalloc((void**)&b.d_cta, sizeof(int64_t) * cta.size()));
   CUDA_TRY(cudaMemcpy(b.d_cta, cta.data(), sizeof(int64_t) * cta.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc((void**)&b.d_red, sizeof(RedTask) * std::max<size_t>(1, reds.size())));
+  if (!reds.empty())
+    CUDA_TRY(cudaMemcpy(b.d_red, reds.data(), sizeof(RedTask) * reds.size(),
+                        cudaMemcpyHostToDevice));
   CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-  for (const Phase& ph : b.phases) {
-    if (!mma)
-      stream_gemm_kernel<8><<<ph.n_cta, kStreamThreads, kStreamSmem, p->stream>>>(
-          b.d_recs, b.d_cta + ph.cta_off, b.d_arena);
-    else if (kb == 8)
+  for (size_t k = 0; k < b.phases.size(); ++k) {
+    const Phase& ph = b.phases[k];
+    const auto& rr = b.red[k];
+    if (rr.second > 0) {
+      const int grid = std::min<int>(rr.second, 148 * 4);
+      if (kb == 8)
+        reduce_partials_kernel<8><<<grid, 256, 0, p->stream>>>(b.d_red + rr.first, rr.second,
+                                                               b.d_arena);
+      else
+        reduce_partials_kernel<16><<<grid, 256, 0, p->stream>>>(b.d_red + rr.first, rr.second,
+                                                                b.d_arena);
+    }
+    if (ph.task_end == ph.task_begin) continue;
+    if (kb == 8)
       stream_mma_kernel<8><<<ph.n_cta, kMmaThreads, kMmaSmem, p->stream>>>(
           b.d_recs, b.d_cta + ph.cta_off, b.d_arena);
     else
@@ -1092,6 +1233,10 @@ int ensure_batched(h2g_plan* p, int which) {
   }
   CUDA_TRY(cudaStreamEndCapture(p->stream, &b.graph));
   CUDA_TRY(cudaGraphInstantiate(&b.exec, b.graph, 0));
+  int launches = 0;
+  for (size_t k = 0; k < b.phases.size(); ++k)
+    launches += (b.red[k].second > 0) + (b.phases[k].task_end > b.phases[k].task_begin);
+  b.launches = launches;
   p->workspace_bytes += sizeof(double) * slots + sizeof(ChunkRec) * recs.size();
   b.ready = true;
   return H2G_OK;
@@ -1099,7 +1244,8 @@ int ensure_batched(h2g_plan* p, int which) {
 
 // Engine for nrhs right-hand sides: 16-wide passes when more than 8 remain.
 inline int batch_which(const h2g_plan* p, int64_t nrhs) {
-  return (!p->batch_dfma && nrhs > 8) ? 1 : 0;
+  (void)p;
+  return nrhs > 8 ? 1 : 0;
 }
 
 int matvec_impl(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nrhs, int64_t ld,
@@ -1272,8 +1418,11 @@ int h2g_launches_per_matvec(const h2g_plan* p, int64_t nrhs) {
   if (!p) return 0;
   if (nrhs > 1 && p->engine == 1 && p->use_batched) {
     int total = 0;
-    for (int64_t c0 = 0; c0 < nrhs; c0 += kBatchKB[batch_which(p, nrhs - c0)])
-      total += (int)p->sched.phases.size() + 2;
+    for (int64_t c0 = 0; c0 < nrhs;) {
+      const int w = batch_which(p, nrhs - c0);
+      total += (p->bat[w].ready ? p->bat[w].launches : (int)p->sched.phases.size()) + 2;
+      c0 += kBatchKB[w];
+    }
     return total;
   }
   return (int)((p->phases.size() + 2) * (nrhs < 1 ? 1 : nrhs));

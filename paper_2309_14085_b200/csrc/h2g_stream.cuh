@@ -59,6 +59,7 @@ namespace h2g {
 #define H2G_CHUNK_A 4096
 #endif
 constexpr int kLastOfTask = 1;
+constexpr int kStridedRun = 2;                // record flag: one bulk copy per column
 constexpr int kConsumers = H2G_CONSUMERS;     // consumer warps per CTA
 constexpr int kStreamThreads = 32 * (1 + kConsumers);
 constexpr int kCtasPerSm = H2G_CTAS_PER_SM;   // independent pipelines per SM
@@ -147,6 +148,29 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           "r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Stage a chunk's operator data: either the record's explicit copy list
+// (lane k issues copy k) or, for a STRIDED RUN (columns of a larger matrix,
+// lda != m), one bulk copy per column: lane k copies column k (16-byte
+// aligned start, so odd offsets carry a one-double shift) to k * ldas.
+// copies[0] then holds {address of A(0, 0), lda, m}.
+__device__ __forceinline__ void issue_operator_copies(const ChunkRec& h, char* st, uint64_t* bar,
+                                                      int lane) {
+  if (h.flags & kStridedRun) {
+    if (lane < h.ncols) {
+      const CopyDesc cd = h.copies[0];
+      const int64_t lda = cd.dst;
+      const int64_t col = (int64_t)lane * lda;
+      const int sh = (int)((h.a_shift + col) & 1);
+      const char* src = reinterpret_cast<const char*>(cd.src) + 8 * (col - sh);
+      bulk_g2s(st + 8 * (int64_t)lane * h.ldas, src, (uint32_t)((8 * (sh + (int)cd.bytes) + 15) & ~15),
+               bar);
+    }
+  } else if (lane < h.n_copies) {
+    const CopyDesc cd = h.copies[lane];
+    bulk_g2s(st + cd.dst, reinterpret_cast<const void*>(cd.src), cd.bytes, bar);
+  }
 }
 
 // ---------------------------------------------------------------- consumer
@@ -240,191 +264,6 @@ __device__ __forceinline__ void consume_stage(const double* __restrict__ As, int
 #pragma unroll
     for (int u = 1; u < U; ++u) tsum += r[u][j];
     acc[j] += tsum;
-  }
-}
-
-// Batched RHS (KB right-hand sides per slot): lanes own rows, every operator
-// entry is loaded from shared memory once and used KB times; X[c][0..KB) is a
-// broadcast LDS.128 stream.  acc[j][b] holds row lane + 32 j, RHS b.
-template <int J, int KB>
-__device__ __forceinline__ void consume_batched(const double* __restrict__ As, int ldas, int ncols,
-                                                const double* __restrict__ Xs, int lane,
-                                                double (&acc)[8][KB]) {
-  const double* base = As + lane;
-#pragma unroll 2
-  for (int c = 0; c < ncols; ++c) {
-    double a[J];
-#pragma unroll
-    for (int j = 0; j < J; ++j) a[j] = base[c * ldas + 32 * j];
-    const double* xc = Xs + c * KB;
-    double xv[KB];
-#pragma unroll
-    for (int b = 0; b < KB; b += 2) {
-      const double2 t = *reinterpret_cast<const double2*>(xc + b);
-      xv[b] = t.x;
-      xv[b + 1] = t.y;
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j)
-#pragma unroll
-      for (int b = 0; b < KB; ++b) acc[j][b] = fma(a[j], xv[b], acc[j][b]);
-  }
-}
-
-// Batched-RHS engine: same producer/ring/records as stream_gemv_kernel, the
-// producer also stages each chunk's X (KB values per column, 64-byte aligned
-// arena slots) by TMA; owned tasks only.
-template <int KB>
-__global__ void __launch_bounds__(kStreamThreads, kCtasPerSm)
-stream_gemm_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__ cta_begin,
-                   double* arena) {
-  extern __shared__ __align__(128) double smem[];
-  double* ring = smem;
-  ChunkRec* rring = reinterpret_cast<ChunkRec*>(smem + kRing + kConsumers * kXStrip);
-  uint64_t* full = reinterpret_cast<uint64_t*>(rring + kRecRing);
-  uint64_t* empty = full + kSlots;
-  uint64_t* recbar = empty + kSlots;
-  int* slot_off = reinterpret_cast<int*>(recbar + kRecRing);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int64_t cb = cta_begin[blockIdx.x];
-  const int n = (int)(cta_begin[blockIdx.x + 1] - cb);
-  const ChunkRec* my = recs + cb;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kSlots; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int r = 0; r < kRecRing; ++r) mbar_init(&recbar[r], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == 0) {
-    int oldest = 0, head = 0, tail = 0;
-    if (lane == 0)
-      for (int j = 0; j < kRecAhead && j < n; ++j) {
-        mbar_arrive_expect_tx(&recbar[j], sizeof(ChunkRec));
-        bulk_g2s(&rring[j], my + j, sizeof(ChunkRec), &recbar[j]);
-      }
-    for (int i = 0; i < n; ++i) {
-      const int s = i % kSlots;
-      const int r = i % kRecRing;
-      mbar_wait(&recbar[r], (uint32_t)(i / kRecRing) & 1u);
-      const ChunkRec& h = rring[r];
-      int off = 0;
-      if (lane == 0) {
-        const int need = h.extent;
-        auto release_oldest = [&]() {
-          mbar_wait(&empty[oldest % kSlots], (uint32_t)(oldest / kSlots) & 1u);
-          ++oldest;
-          tail = oldest < i ? slot_off[oldest % kSlots] : head;
-        };
-        while (i - oldest >= kSlots) release_oldest();
-        while (true) {
-          if (oldest == i) {
-            head = tail = 0;
-            off = 0;
-            break;
-          }
-          if (head >= tail) {
-            if (kRing - head >= need) { off = head; break; }
-            if (tail > need) { off = 0; break; }
-          } else if (tail - head > need) {
-            off = head;
-            break;
-          }
-          release_oldest();
-        }
-        head = off + need;
-        slot_off[s] = off;
-        const int j = i + kRecAhead;
-        if (j < n) {
-          const int rj = j % kRecRing;
-          mbar_arrive_expect_tx(&recbar[rj], sizeof(ChunkRec));
-          bulk_g2s(&rring[rj], my + j, sizeof(ChunkRec), &recbar[rj]);
-        }
-        mbar_arrive_expect_tx(&full[s], h.bytes_a + h.bytes_x);
-      }
-      off = __shfl_sync(0xffffffffu, off, 0);
-      char* st = reinterpret_cast<char*>(ring + off);
-      if (lane < h.n_copies) {  // operator copies
-        const CopyDesc cd = h.copies[lane];
-        bulk_g2s(st + cd.dst, reinterpret_cast<const void*>(cd.src), cd.bytes, &full[s]);
-      }
-      if (lane < h.n_seg) {  // X segment copies: KB doubles per column, 64-byte aligned
-        const int c0 = h.seg_c0[lane], c1 = h.seg_c0[lane + 1];
-        bulk_g2s(st + 8 * (h.x_base + c0 * KB), reinterpret_cast<const void*>(h.seg_src[lane]),
-                 (uint32_t)(8 * KB * (c1 - c0)), &full[s]);
-      }
-      __syncwarp();
-    }
-    return;
-  }
-
-  const int cw = warp - 1;
-  double acc[8][KB];
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-#pragma unroll
-    for (int b = 0; b < KB; ++b) acc[j][b] = 0.0;
-  for (int i = cw; i < n; i += kConsumers) {
-    const int s = i % kSlots;
-    mbar_wait(&recbar[i % kRecRing], (uint32_t)(i / kRecRing) & 1u);
-    const ChunkRec& h = rring[i % kRecRing];
-    const int m = h.m;
-    const int ncols = h.ncols;
-    const int flags = h.flags;
-    const int ldas = h.ldas;
-    const int a_shift = h.a_shift;
-    const int odd = h.odd_lda;
-    const int x_base = h.x_base;
-    const int64_t y_off = h.y_off;
-    mbar_wait(&full[s], (uint32_t)(i / kSlots) & 1u);
-    const double* sA = ring + slot_off[s];
-    const double* Xs = sA + x_base;
-    if (!odd) {
-      const double* As = sA + a_shift;
-      const int J = (m + 31) >> 5;
-      if (J == 1)
-        consume_batched<1, KB>(As, ldas, ncols, Xs, lane, acc);
-      else if (J == 2)
-        consume_batched<2, KB>(As, ldas, ncols, Xs, lane, acc);
-      else if (J <= 4)
-        consume_batched<4, KB>(As, ldas, ncols, Xs, lane, acc);
-      else
-        consume_batched<8, KB>(As, ldas, ncols, Xs, lane, acc);
-    } else {
-      for (int c = 0; c < ncols; ++c) {
-        const double* col = sA + (size_t)c * ldas + ((a_shift + c) & 1);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int rr = lane + 32 * j;
-          if (rr < m) {
-            const double av = col[rr];
-#pragma unroll
-            for (int b = 0; b < KB; ++b) acc[j][b] = fma(av, Xs[c * KB + b], acc[j][b]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (flags & kLastOfTask) {
-      double* y = arena + y_off * KB;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int rr = lane + 32 * j;
-        if (rr < m)
-#pragma unroll
-          for (int b = 0; b < KB; b += 2)
-            *reinterpret_cast<double2*>(y + rr * KB + b) = make_double2(acc[j][b], acc[j][b + 1]);
-#pragma unroll
-        for (int b = 0; b < KB; ++b) acc[j][b] = 0.0;
-      }
-    }
   }
 }
 
@@ -613,10 +452,7 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
       }
       off = __shfl_sync(0xffffffffu, off, 0);
       char* st = reinterpret_cast<char*>(ring + off);
-      if (lane < h.n_copies) {
-        const CopyDesc cd = h.copies[lane];
-        bulk_g2s(st + cd.dst, reinterpret_cast<const void*>(cd.src), cd.bytes, &full[s]);
-      }
+      issue_operator_copies(h, st, &full[s], lane);
       if (lane < h.n_seg) {
         const int c0 = h.seg_c0[lane], c1 = h.seg_c0[lane + 1];
         bulk_g2s(st + 8 * (h.x_base + c0 * KB), reinterpret_cast<const void*>(h.seg_src[lane]),
@@ -828,11 +664,7 @@ stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict_
         mbar_arrive_expect_tx(&full[s], h.bytes_a);
       }
       off = __shfl_sync(0xffffffffu, off, 0);
-      if (lane < h.n_copies) {  // lane k issues operator copy k (TMA bulk)
-        const CopyDesc cd = h.copies[lane];
-        char* st = reinterpret_cast<char*>(ring + off);
-        bulk_g2s(st + cd.dst, reinterpret_cast<const void*>(cd.src), cd.bytes, &full[s]);
-      }
+      issue_operator_copies(h, reinterpret_cast<char*>(ring + off), &full[s], lane);
       __syncwarp();
     }
     return;

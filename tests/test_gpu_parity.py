@@ -136,3 +136,25 @@ def test_batched_engine_edge_widths(reps):
         for j in range(k):
             assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= TOL
     assert np.all(rep.matmat(np.zeros((op.N, 16))) == 0)
+
+
+@pytest.mark.parametrize("name", ["g2d_log_bigleaf_h2star", "g2d_log_h2plusH", "g3d_lap_h2star"])
+def test_split_k_pieces(monkeypatch, name):
+    """Heavy tasks cut into split-K pieces and reduce phases (forced by a
+    tiny piece floor): single- and 16-RHS results still match the reference."""
+    from paper_2309_14085_b200.gpu_rep import GpuHierRep
+    op, z, meta = load_golden(name)
+    plain = GpuHierRep(op)
+    n_plain = plain.stats()["n_phases"]
+    plain.close()
+    monkeypatch.setenv("H2G_SPLIT_MIN_BYTES", "2048")
+    rep = GpuHierRep(op)
+    try:
+        assert rep.stats()["n_phases"] > n_plain
+        assert rel_err(rep.matvec(z["q"]), z["phi_ref"]) <= TOL
+        Q = np.random.default_rng(5).standard_normal((op.N, 16))
+        Phi = rep.matmat(Q)
+        for j in (0, 15):
+            assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= TOL
+    finally:
+        rep.close()
