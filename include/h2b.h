@@ -33,6 +33,7 @@ extern "C" {
 
 enum { H2B_VARIANT_H2STAR_BT = 0, H2B_VARIANT_H2PLUSH_STAR = 1 };
 enum { H2B_KERNEL_LOG2D = 0, H2B_KERNEL_LAP3D = 1, H2B_KERNEL_GAUSSIAN = 2 };
+enum { H2B_SKIP_NEAR = 1, H2B_SKIP_M2L = 2 };
 enum { H2B_OK = 0, H2B_ERR_INVALID_ARG = 1, H2B_ERR_SINGULAR = 2, H2B_ERR_OOM = 3 };
 
 typedef struct h2b_params {
@@ -51,7 +52,9 @@ typedef struct h2b_params {
   double eps_far;        /* NCA tolerance of the far channel */
   double eps_ver;        /* NCA / ACA tolerance of the vertex leg */
   int32_t n_threads;     /* 0 = OpenMP default */
-  int32_t reserved;
+  int32_t skip_blocks;   /* H2B_SKIP_* mask: blocks NOT stored (offset -1 in the export,
+                            evaluated on the device: h2g.h recompute path); they still
+                            count in mem_scalars (engine.py:315 counts lazy near blocks) */
 } h2b_params;
 
 typedef struct h2b_result h2b_result;
@@ -61,7 +64,8 @@ enum { H2B_I32 = 0, H2B_I64 = 1, H2B_F64 = 2 };
 
 int h2b_build(const h2b_params* params, h2b_result** out);
 /* Named arrays of the packed export (packed.py field names, channel fields
- * prefixed "ch0_"/"ch1_").  The pointer stays valid until h2b_free. */
+ * prefixed "ch0_"/"ch1_", incl. the NCA pivots "chK_piv_in_ptr/_piv_in/
+ * _piv_out_ptr/_piv_out" as tree positions).  The pointer stays valid until h2b_free. */
 int h2b_get_array(const h2b_result* r, const char* name, const void** ptr, int64_t* len,
                   int32_t* dtype);
 /* Scalars: "kappa", "n_channels", "mem_scalars", "n_clusters". */

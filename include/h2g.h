@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define H2G_ABI_VERSION 2
+#define H2G_ABI_VERSION 3
 
 enum {
   H2G_OK = 0,
@@ -61,7 +61,16 @@ typedef struct h2g_channel_desc {
   const int64_t* l2l_off;     /* [n_clusters] r_in(c) x r_in(P)      ops.l2l[(c, P)]   keyed by child c */
   const int64_t* m2l_rowptr;  /* [n_clusters + 1] CSR by target X                      */
   const int32_t* m2l_src;     /* [nnz] source Y, lists_fn order (partition.py:133-136) */
-  const int64_t* m2l_off;     /* [nnz] r_in(X) x r_out(Y)            ops.m2l[(X, Y)]   */
+  const int64_t* m2l_off;     /* [nnz] r_in(X) x r_out(Y)            ops.m2l[(X, Y)]
+                                 -1 = not stored: evaluated on the device as
+                                 K[t_i(X), s_o(Y)] (engine.py:176-179) */
+  /* NCA pivots (PivotQuad.t_i / s_o, lowrank.py:45-59) as TREE POSITIONS, CSR
+   * by cluster (piv_in: r_in entries, piv_out: r_out entries).  Needed only
+   * for M2L recompute; NULL otherwise. */
+  const int64_t* piv_in_ptr;  /* [n_clusters + 1] */
+  const int64_t* piv_in;      /* t_i(X) */
+  const int64_t* piv_out_ptr; /* [n_clusters + 1] */
+  const int64_t* piv_out;     /* s_o(X) */
 } h2g_channel_desc;
 
 /* The packed export (paper_2309_14085_b200/packed.py, SURVEY.md §8(a')). */
@@ -89,10 +98,32 @@ typedef struct h2g_export_desc {
   /* near field (engine.py:260-268): CSR by target leaf */
   const int64_t* near_rowptr; /* [n_clusters + 1] */
   const int32_t* near_src;    /* [nnz] */
-  const int64_t* near_off;    /* [nnz] n_X x n_Y column-major */
+  const int64_t* near_off;    /* [nnz] n_X x n_Y column-major; -1 = not stored
+                                 (reference store_near=False, engine.py:260-268:
+                                 kernel.block(t^X, t^Y) evaluated on the device) */
   int64_t blob_len;           /* doubles */
   const double* blob;         /* all operator matrices */
+  /* ---- kernel-evaluation ("recompute", P2P-style) path, ABI 3 ----
+   * The M2L blocks are raw kernel blocks K[t_i(X), s_o(Y)] and the near
+   * blocks K[t^X, t^Y] (engine.py:176-179, 309-318), so the device can
+   * evaluate them from point coordinates instead of streaming them.
+   * Kernel rules follow Kernel.block (kernels.py:36-57). */
+  const double* points_tree;  /* [N x dim] coordinates in tree order (NULL: no recompute) */
+  int32_t kernel_type;        /* H2G_KERNEL_* (-1: unknown -> no recompute) */
+  int32_t has_diag;           /* Kernel.diag is not None */
+  double zero_value;          /* value at r == 0, i != j */
+  double diag;                /* value at i == j (if has_diag) */
+  double shift;               /* added at i == j */
+  double sigma;               /* Gaussian width */
+  int32_t recompute;          /* H2G_RECOMPUTE_* mask: evaluate these blocks even where stored */
+  int32_t pad0;
+  double m2l_recompute_share; /* (0, 1]: share of the eligible M2L work (by bytes, per
+                                 level) evaluated on the fp64 pipe while the rest streams
+                                 concurrently from HBM; 0 or 1 = all of it */
 } h2g_export_desc;
+
+enum { H2G_KERNEL_LOG2D = 0, H2G_KERNEL_LAP3D = 1, H2G_KERNEL_GAUSSIAN = 2 };
+enum { H2G_RECOMPUTE_NEAR = 1, H2G_RECOMPUTE_M2L = 2 };
 
 typedef struct h2g_plan h2g_plan;
 

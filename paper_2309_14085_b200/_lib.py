@@ -11,7 +11,10 @@ import os
 
 LIBDIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 
-H2G_ABI_VERSION = 2
+H2G_ABI_VERSION = 3
+H2G_RECOMPUTE_NEAR = 1
+H2G_RECOMPUTE_M2L = 2
+H2G_KERNELS = {"log2d": 0, "lap3d": 1, "gaussian": 2}
 H2G_OK = 0
 H2G_ERR_LENGTH_MISMATCH = 1
 
@@ -23,7 +26,8 @@ P_F64 = C.POINTER(C.c_double)
 class ChannelDesc(C.Structure):
     _fields_ = [("r_in", P_I32), ("r_out", P_I32), ("p2m_off", P_I64), ("l2p_off", P_I64),
                 ("m2m_off", P_I64), ("l2l_off", P_I64), ("m2l_rowptr", P_I64),
-                ("m2l_src", P_I32), ("m2l_off", P_I64)]
+                ("m2l_src", P_I32), ("m2l_off", P_I64), ("piv_in_ptr", P_I64),
+                ("piv_in", P_I64), ("piv_out_ptr", P_I64), ("piv_out", P_I64)]
 
 
 class ExportDesc(C.Structure):
@@ -34,7 +38,10 @@ class ExportDesc(C.Structure):
                 ("blr_rowptr", P_I64), ("blr_src", P_I32), ("blr_rank", P_I32),
                 ("blr_u_off", P_I64), ("blr_v_off", P_I64), ("near_rowptr", P_I64),
                 ("near_src", P_I32), ("near_off", P_I64), ("blob_len", C.c_int64),
-                ("blob", P_F64)]
+                ("blob", P_F64), ("points_tree", P_F64), ("kernel_type", C.c_int32),
+                ("has_diag", C.c_int32), ("zero_value", C.c_double), ("diag", C.c_double),
+                ("shift", C.c_double), ("sigma", C.c_double), ("recompute", C.c_int32),
+                ("pad0", C.c_int32), ("m2l_recompute_share", C.c_double)]
 
 
 class PlanStats(C.Structure):

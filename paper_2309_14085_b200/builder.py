@@ -20,7 +20,7 @@ import os
 
 import numpy as np
 
-from .packed import CHANNEL_FIELDS, PackedChannel, PackedOperator
+from .packed import CHANNEL_FIELDS, PIVOT_FIELDS, PackedChannel, PackedOperator
 
 LIBDIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 VARIANTS = {"h2star-bt": 0, "h2plusH-star": 1}
@@ -39,7 +39,7 @@ class H2bParams(C.Structure):
                 ("kernel", C.c_int32), ("has_diag", C.c_int32), ("zero_value", C.c_double),
                 ("diag", C.c_double), ("shift", C.c_double), ("sigma", C.c_double),
                 ("eps_far", C.c_double), ("eps_ver", C.c_double), ("n_threads", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("skip_blocks", C.c_int32)]
 
 
 H2B_SYMBOLS = ("h2b_build", "h2b_get_array", "h2b_get_scalar", "h2b_get_timing", "h2b_free",
@@ -108,8 +108,14 @@ class _Result:
 def build_variant(variant: str, points, kernel: str = "log2d", n_max: int = 64,
                   eps: float = 1e-8, eps_far: float = None, eps_ver: float = None,
                   n_threads: int = 0, zero_value=None, diag=None, shift=None, sigma=None,
-                  copy_blob: bool = False) -> PackedOperator:
-    """Native build_variant (engine.py:325-373) -> PackedOperator."""
+                  copy_blob: bool = False, store: str = "near,m2l") -> PackedOperator:
+    """Native build_variant (engine.py:325-373) -> PackedOperator.
+
+    ``store`` names the raw kernel blocks kept in the blob ("near", "m2l");
+    the others are exported with offset -1 and evaluated on the device from
+    the points / NCA pivots (the reference's store_near=False,
+    engine.py:260-268, extended to M2L = K[t_i, s_o], engine.py:176-179).
+    The pivots are always exported."""
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant '{variant}'")
     if kernel not in KERNELS:
@@ -140,6 +146,10 @@ def build_variant(variant: str, points, kernel: str = "log2d", n_max: int = 64,
     p.eps_far = float(eps_far)
     p.eps_ver = float(eps_ver)
     p.n_threads = int(n_threads)
+    kinds = {k for k in store.replace(" ", "").split(",") if k}
+    if kinds - {"near", "m2l"}:
+        raise ValueError(f"store: unknown block kinds {sorted(kinds - {'near', 'm2l'})}")
+    p.skip_blocks = (0 if "near" in kinds else 1) | (0 if "m2l" in kinds else 2)
     h = C.c_void_p()
     rc = L.h2b_build(C.byref(p), C.byref(h))
     if rc:
@@ -149,7 +159,8 @@ def build_variant(variant: str, points, kernel: str = "log2d", n_max: int = 64,
         raise RuntimeError(f"h2b_build failed ({rc}): {msg}")
     R = _Result(L, h)
     nch = R.scalar("n_channels")
-    chans = [PackedChannel(**{f: R.array(f"ch{i}_{f}") for f in CHANNEL_FIELDS})
+    chans = [PackedChannel(**{f: R.array(f"ch{i}_{f}") for f in CHANNEL_FIELDS},
+                           **{f: R.array(f"ch{i}_{f}") for f in PIVOT_FIELDS})
              for i in range(nch)]
     blob = R.array("blob", copy=copy_blob)
     op = PackedOperator(

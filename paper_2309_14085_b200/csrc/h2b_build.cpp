@@ -710,7 +710,10 @@ struct Blob {
 };
 
 // engine.py:133-187: sizes first (offsets in the exporter's order), then fill
-void layout_channel(const Tree& T, Channel& ch, Blob& B) {
+// store_m2l = false: M2L blocks are not stored (offset -1, evaluated on the
+// device from the pivots); their scalars still count in mem_scalars.
+int64_t layout_channel(const Tree& T, Channel& ch, Blob& B, bool store_m2l = true) {
+  int64_t unstored = 0;
   const int64_t nc = T.nc();
   const int k = T.kappa;
   ch.p2m_off.assign(nc, -1);
@@ -744,11 +747,14 @@ void layout_channel(const Tree& T, Channel& ch, Blob& B) {
     if (Q[x].t_i.size())
       for (int64_t y : L[x])
         if (Q[y].t_o.size()) {
+          const int64_t n = (int64_t)Q[x].t_i.size() * Q[y].t_o.size();
           ch.m2l_src.push_back((int32_t)y);
-          ch.m2l_off.push_back(B.take((int64_t)Q[x].t_i.size() * Q[y].t_o.size()));
+          ch.m2l_off.push_back(store_m2l ? B.take(n) : -1);
+          if (!store_m2l) unstored += n;
         }
     ch.m2l_rowptr[x + 1] = (int64_t)ch.m2l_src.size();
   }
+  return unstored;
 }
 
 void fill_channel(const Tree& T, const Kernel& K, const Channel& ch, double* blob) {
@@ -806,6 +812,7 @@ void fill_channel(const Tree& T, const Kernel& K, const Channel& ch, double* blo
         }
         // M2L is the raw kernel block K[t_i(X), s_o(Y)] (engine.py:176-179)
         for (int64_t kk = ch.m2l_rowptr[x]; kk < ch.m2l_rowptr[x + 1]; ++kk) {
+          if (ch.m2l_off[kk] < 0) continue;  // evaluated on the device
           const Quad& yq = Q[ch.m2l_src[kk]];
           K.block_cm(q.t_i.data(), ri, yq.s_o.data(), (int64_t)yq.s_o.size(),
                      blob + ch.m2l_off[kk], ri);
@@ -887,8 +894,11 @@ int build_impl(const h2b_params* P, h2b_result** out) {
   R->timing["pivots"] = now() - t0;
 
   Blob B;
-  for (auto& ch : chans) layout_channel(T, ch, B);
-  int64_t mem = B.len;  // channel operators (non-symmetric: no shared views)
+  const bool store_near = (P->skip_blocks & H2B_SKIP_NEAR) == 0;
+  const bool store_m2l = (P->skip_blocks & H2B_SKIP_M2L) == 0;
+  int64_t unstored = 0;
+  for (auto& ch : chans) unstored += layout_channel(T, ch, B, store_m2l);
+  int64_t mem = B.len + unstored;  // channel operators (non-symmetric: no shared views)
 
   // BLR leg (blr.py:46-69, lists="ver", include_near=False)
   t0 = now();
@@ -949,7 +959,7 @@ int build_impl(const h2b_params* P, h2b_result** out) {
         mem += T.size(x) * T.size(y);
         if (T.size(x) && T.size(y)) {
           near_src.push_back((int32_t)y);
-          near_off.push_back(B.take(T.size(x) * T.size(y)));
+          near_off.push_back(store_near ? B.take(T.size(x) * T.size(y)) : -1);
         }
       }
     near_rowptr[x + 1] = (int64_t)near_src.size();
@@ -1031,6 +1041,7 @@ int build_impl(const h2b_params* P, h2b_result** out) {
       for (int64_t kk = near_rowptr[x]; kk < near_rowptr[x + 1]; ++kk) nx_of[kk] = x;
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t kk = 0; kk < (int64_t)near_src.size(); ++kk) {
+      if (near_off[kk] < 0) continue;  // evaluated on the device (store_near=False)
       const int64_t x = nx_of[kk], y = near_src[kk];
       K.block_cm(T.perm.data() + T.st[x], T.size(x), T.perm.data() + T.st[y], T.size(y),
                  blob.data() + near_off[kk], T.size(x));
@@ -1039,6 +1050,8 @@ int build_impl(const h2b_params* P, h2b_result** out) {
   R->timing["near"] = now() - t0;
 
   // ---- outputs (packed.py field names)
+  std::vector<int64_t> inv_perm(T.N);
+  for (int64_t i = 0; i < T.N; ++i) inv_perm[T.perm[i]] = i;
   R->i64["perm"] = T.perm;
   R->i64["level_offset"] = T.lo;
   R->i64["cl_start"] = T.st;
@@ -1055,6 +1068,18 @@ int build_impl(const h2b_params* P, h2b_result** out) {
     R->i64[p + "m2l_rowptr"] = ch.m2l_rowptr;
     R->i32[p + "m2l_src"] = ch.m2l_src;
     R->i64[p + "m2l_off"] = ch.m2l_off;
+    // NCA pivots t_i / s_o as tree positions (M2L evaluation on the device)
+    std::vector<int64_t> ip(nc + 1, 0), op(nc + 1, 0), iv, ov;
+    for (int64_t x = 0; x < nc; ++x) {
+      for (int64_t g : ch.quads[x].t_i) iv.push_back(inv_perm[g]);
+      for (int64_t g : ch.quads[x].s_o) ov.push_back(inv_perm[g]);
+      ip[x + 1] = (int64_t)iv.size();
+      op[x + 1] = (int64_t)ov.size();
+    }
+    R->i64[p + "piv_in_ptr"] = std::move(ip);
+    R->i64[p + "piv_in"] = std::move(iv);
+    R->i64[p + "piv_out_ptr"] = std::move(op);
+    R->i64[p + "piv_out"] = std::move(ov);
   }
   R->i64["blr_rowptr"] = blr_rowptr;
   R->i32["blr_src"] = blr_src;

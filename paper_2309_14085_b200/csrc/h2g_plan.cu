@@ -33,6 +33,7 @@
 
 #include "../../include/h2g.h"
 #include "h2g_kernels.cuh"
+#include "h2g_p2p.cuh"
 #include "h2g_stream.cuh"
 
 using namespace h2g;
@@ -65,6 +66,11 @@ struct Phase {
   int64_t cta_off = 0;                   // streaming engine: CTA ranges at d_cta[cta_off ..]
   int32_t n_cta = 0;
   int32_t split = 0;                     // 1: all warps per chunk (narrow phase)
+  // tasks [task_begin, stream_end) run on the streaming engine, [stream_end,
+  // task_end) (tasks with kernel-evaluated terms) on the P2P engine
+  int64_t stream_end = -1;               // -1: all tasks stream
+  int32_t hybrid = 0;
+  int64_t p2p_off = 0;                   // first P2PTask of the phase                    // both engines concurrently (1 stream CTA per SM)
 };
 
 // Multi-GPU ownership: subtrees at level `level` are split into
@@ -85,10 +91,15 @@ struct Shard {
   int owner(int64_t m, int l) const { return owner_of_subtree(m >> (dim * (l - level))); }
 };
 
+struct Rec4 {  // point record of the P2P engine (device double4)
+  double x, y, z, w;
+};
+
 struct HostSchedule {
   std::vector<Task> tasks;
   std::vector<Term> terms;
   std::vector<Phase> phases;
+  std::vector<Rec4> recs;  // [0, N): points in tree order, then pivot runs
   // terms of the task currently being built (before row splitting)
   std::vector<Term> cur;
 };
@@ -104,6 +115,10 @@ constexpr int64_t kSplitCtas = 4 * 296;       // pieces per phase: ~4 per persis
 constexpr int64_t kSplitMinBytes = 1 << 20;   // never cut below 1 MB pieces
 // batched-RHS engines: 8 or 16 right-hand sides per operator pass
 constexpr int kBatchKB[2] = {8, 16};
+// hybrid phases: a streaming CTA asks for more than half an SM's shared
+// memory, so exactly one lands per SM and a P2P CTA fits beside it
+constexpr size_t kStreamSmemHybrid = 118 * 1024;
+static_assert(kStreamSmemHybrid >= kStreamSmem, "hybrid smem below the engine's need");
 
 struct HostChunk {      // streaming chunk before decoding into a ChunkRec
   int64_t a_off;        // offset (doubles) of the first operator entry (blob or arena)
@@ -174,6 +189,19 @@ struct h2g_plan {
     int launches = 0;               // kernels per pass (graph)
   } bat[2];                         // KB = kBatchKB[i]
   bool use_batched = true;  // nrhs > 1 through the batched engine (H2G_BATCHED=0: column loop)
+  // P2P (kernel-evaluation) engine
+  double4* d_recs4 = nullptr;  // point records
+  int64_t n_recs = 0;
+  P2PTask* d_p2p_tasks = nullptr;
+  Term* d_p2p_terms = nullptr;     // stored terms of the P2P tasks
+  P2PChunk* d_p2p_chunks = nullptr;
+  int* d_ctr = nullptr;        // 2 task counters per phase
+  P2PKernel kp{};
+  int kernel_type = -1;
+  int dim = 2;
+  bool has_p2p = false;
+  cudaStream_t stream2 = nullptr;  // hybrid phases: the P2P engine's branch of the graph
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* d_hq = nullptr;    // host-call staging (h2g_matvec_host)
   double* d_hphi = nullptr;
   size_t h_cap = 0;
@@ -183,7 +211,9 @@ namespace {
 
 // Emit the task being built (rows y[0:m)), splitting rows into <= kMaxRows
 // pieces; every piece keeps the same terms shifted by its first row.
-void emit_task(HostSchedule& s, int64_t y_off, int64_t m, int64_t& bytes) {
+// A task with kernel-evaluated terms (P2P engine) names its row records:
+// row_rec = record of row 0 (Task.pad); -1 for a plain GEMV task.
+void emit_task(HostSchedule& s, int64_t y_off, int64_t m, int64_t& bytes, int64_t row_rec = -1) {
   for (int64_t r0 = 0; r0 < m; r0 += kMaxRows) {
     const int32_t mm = (int32_t)std::min<int64_t>(kMaxRows, m - r0);
     Task t;
@@ -192,12 +222,12 @@ void emit_task(HostSchedule& s, int64_t y_off, int64_t m, int64_t& bytes) {
     t.t_begin = (int32_t)s.terms.size();
     for (const Term& tm : s.cur) {
       Term u = tm;
-      u.a_off += r0;
+      if (u.a_space != kRecompute) u.a_off += r0;  // evaluated terms: rows shift via Task.pad
       s.terms.push_back(u);
       bytes += 8LL * mm * tm.ncols;
     }
     t.t_end = (int32_t)s.terms.size();
-    t.pad = 0;
+    t.pad = row_rec >= 0 ? (int32_t)(row_rec + r0) : 0;
     s.tasks.push_back(t);
   }
   for (const Term& tm : s.cur) bytes += 8LL * tm.ncols;  // x reads
@@ -216,6 +246,25 @@ void add_term(HostSchedule& s, int64_t a_off, int64_t x_off, int64_t lda, int64_
   t.a_space = a_space;
   t.pad = 0;
   s.cur.push_back(t);
+}
+
+// kernel-evaluated block K[rows of the task, records rec_off .. rec_off+ncols) * x
+void add_rc_term(HostSchedule& s, int64_t rec_off, int64_t x_off, int64_t ncols, bool self) {
+  if (ncols <= 0) return;
+  Term t;
+  t.a_off = rec_off;
+  t.x_off = x_off;
+  t.lda = 0;
+  t.ncols = (int32_t)ncols;
+  t.a_space = kRecompute;
+  t.pad = self ? 1 : 0;
+  s.cur.push_back(t);
+}
+
+inline bool is_p2p_task(const HostSchedule& s, const Task& t) {
+  for (int32_t k = t.t_begin; k < t.t_end; ++k)
+    if (s.terms[k].a_space == kRecompute) return true;
+  return false;
 }
 
 void begin_phase(HostSchedule& s, int kind, const std::string& name) {
@@ -267,14 +316,14 @@ void split_heavy_tasks(HostSchedule& s, int64_t& slots, int64_t ones_off) {
     for (int32_t k = t.t_begin; k < t.t_end; ++k) c += s.terms[k].ncols;
     return 8 * (int64_t)t.m * c;
   };
-  auto push_task = [&](int64_t y_off, int32_t m, const std::vector<Term>& tm) {
+  auto push_task = [&](int64_t y_off, int32_t m, const std::vector<Term>& tm, int32_t row_rec = 0) {
     Task t;
     t.y_off = y_off;
     t.m = m;
     t.t_begin = (int32_t)terms.size();
     for (const Term& u : tm) terms.push_back(u);
     t.t_end = (int32_t)terms.size();
-    t.pad = 0;
+    t.pad = row_rec;
     tasks.push_back(t);
   };
   int64_t min_bytes = kSplitMinBytes;
@@ -291,7 +340,7 @@ void split_heavy_tasks(HostSchedule& s, int64_t& slots, int64_t ones_off) {
       std::vector<Term> tm(s.terms.begin() + t.t_begin, s.terms.begin() + t.t_end);
       const int64_t tb = task_bytes(t);
       if (tb <= thr) {
-        push_task(t.y_off, t.m, tm);
+        push_task(t.y_off, t.m, tm, t.pad);
         continue;
       }
       int64_t cols = 0;
@@ -307,14 +356,14 @@ void split_heavy_tasks(HostSchedule& s, int64_t& slots, int64_t ones_off) {
         while (c0 < u.ncols) {
           const int64_t take = std::min<int64_t>(u.ncols - c0, per - in_piece);
           Term v = u;
-          v.a_off = u.a_off + c0 * u.lda;
+          v.a_off = u.a_space == kRecompute ? u.a_off + c0 : u.a_off + c0 * u.lda;
           v.x_off = u.x_off + c0;
           v.ncols = (int32_t)take;
           cur.push_back(v);
           in_piece += take;
           c0 += take;
           if (in_piece == per) {
-            push_task(part + np * t.m, t.m, cur);
+            push_task(part + np * t.m, t.m, cur, t.pad);
             ++np;
             cur.clear();
             in_piece = 0;
@@ -322,7 +371,7 @@ void split_heavy_tasks(HostSchedule& s, int64_t& slots, int64_t ones_off) {
         }
       }
       if (!cur.empty()) {
-        push_task(part + np * t.m, t.m, cur);
+        push_task(part + np * t.m, t.m, cur, t.pad);
         ++np;
       }
       slots += np * t.m;
@@ -340,6 +389,7 @@ void split_heavy_tasks(HostSchedule& s, int64_t& slots, int64_t ones_off) {
     phases.push_back(main);
     if (!reduces.empty()) {
       Phase red = ph;
+      red.hybrid = 0;
       red.name = ph.name + "_red";
       red.alg_bytes = 0;
       red.task_begin = (int64_t)tasks.size();
@@ -351,6 +401,78 @@ void split_heavy_tasks(HostSchedule& s, int64_t& slots, int64_t ones_off) {
   s.tasks.swap(tasks);
   s.terms.swap(terms);
   s.phases.swap(phases);
+}
+
+// Inside every phase: streaming tasks first, then the P2P tasks (those with
+// kernel-evaluated terms) in decreasing cost order (the P2P engine fetches
+// them dynamically, largest first).
+void partition_engines(HostSchedule& s) {
+  for (Phase& ph : s.phases) {
+    std::vector<Task> st_t, p2p_t;
+    std::vector<double> cost;
+    for (int64_t i = ph.task_begin; i < ph.task_end; ++i) {
+      const Task& t = s.tasks[i];
+      if (is_p2p_task(s, t)) p2p_t.push_back(t);
+      else st_t.push_back(t);
+    }
+    if (p2p_t.empty()) {
+      ph.stream_end = -1;
+      ph.hybrid = 0;
+      continue;
+    }
+    auto tcost = [&](const Task& t) {
+      int64_t c = 0;
+      for (int32_t k = t.t_begin; k < t.t_end; ++k) c += s.terms[k].ncols;
+      return (double)t.m * (double)c;
+    };
+    std::stable_sort(p2p_t.begin(), p2p_t.end(),
+                     [&](const Task& a, const Task& b) { return tcost(a) > tcost(b); });
+    int64_t i = ph.task_begin;
+    for (const Task& t : st_t) s.tasks[i++] = t;
+    ph.stream_end = i;
+    for (const Task& t : p2p_t) s.tasks[i++] = t;
+    ph.hybrid = st_t.empty() ? 0 : 1;
+  }
+}
+
+inline int64_t stream_end_of(const Phase& ph) {
+  return ph.stream_end < 0 ? ph.task_end : ph.stream_end;
+}
+
+// P2P work lists: per task its stored terms (own table) and its evaluated
+// terms cut into <= kP2PChunk-column chunks.
+void build_p2p_lists(const HostSchedule& s, std::vector<Phase>& phases,
+                     std::vector<P2PTask>& pt, std::vector<Term>& pterms,
+                     std::vector<P2PChunk>& pch) {
+  for (Phase& ph : phases) {
+    ph.p2p_off = (int64_t)pt.size();
+    for (int64_t i = stream_end_of(ph); i < ph.task_end; ++i) {
+      const Task& t = s.tasks[i];
+      P2PTask q{};
+      q.y_off = t.y_off;
+      q.m = t.m;
+      q.row_rec = t.pad;
+      q.t_begin = (int32_t)pterms.size();
+      q.k_begin = (int32_t)pch.size();
+      for (int32_t k = t.t_begin; k < t.t_end; ++k) {
+        const Term& tm = s.terms[k];
+        if (tm.a_space != kRecompute) {
+          pterms.push_back(tm);
+          continue;
+        }
+        for (int32_t c0 = 0; c0 < tm.ncols; c0 += kP2PChunk) {
+          P2PChunk c;
+          c.x_off = tm.x_off + c0;
+          c.rec = (int32_t)(tm.a_off + c0);
+          c.n_self = std::min(kP2PChunk, tm.ncols - c0) | (tm.pad ? kSelfBit : 0);
+          pch.push_back(c);
+        }
+      }
+      q.t_end = (int32_t)pterms.size();
+      q.k_end = (int32_t)pch.size();
+      pt.push_back(q);
+    }
+  }
 }
 
 int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const Shard& sh) {
@@ -481,6 +603,61 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
     }
   }
 
+  // ---- kernel-evaluation (P2P) records and what gets evaluated ----
+  // Blocks exported with offset -1 are always evaluated; the recompute mask
+  // asks for stored ones too.  Records: [0, N) the points in tree order (near
+  // rows/columns), then per channel and cluster the runs t_i (M2L rows) and
+  // s_o (M2L columns), coordinates copied from points_tree.
+  const int64_t N = d->n_points;
+  bool need_near = (d->recompute & H2G_RECOMPUTE_NEAR) != 0;
+  bool need_m2l = (d->recompute & H2G_RECOMPUTE_M2L) != 0;
+  for (int64_t k = 0; k < d->near_rowptr[nc]; ++k)
+    if (d->near_off[k] < 0) need_near = true;
+  for (int ch = 0; ch < d->n_channels; ++ch)
+    for (int64_t k = 0; k < d->channels[ch].m2l_rowptr[nc]; ++k)
+      if (d->channels[ch].m2l_off[k] < 0) need_m2l = true;
+  std::vector<std::vector<int64_t>> rin_rec(d->n_channels), rout_rec(d->n_channels);
+  s.recs.clear();
+  if (need_near || need_m2l) {
+    if (!d->points_tree || d->kernel_type < 0 || d->kernel_type > 2)
+      return fail(H2G_ERR_BAD_EXPORT,
+                  "kernel evaluation needs points_tree and a known kernel_type");
+    s.recs.resize(N);
+    for (int64_t i = 0; i < N; ++i) {
+      const double* x = d->points_tree + i * dim;
+      s.recs[i] = Rec4{x[0], dim > 1 ? x[1] : 0.0, dim > 2 ? x[2] : 0.0, 0.0};
+    }
+  }
+  if (need_m2l) {
+    for (int ch = 0; ch < d->n_channels; ++ch) {
+      const h2g_channel_desc& c = d->channels[ch];
+      if (!c.piv_in_ptr || !c.piv_in || !c.piv_out_ptr || !c.piv_out)
+        return fail(H2G_ERR_BAD_EXPORT, "M2L evaluation needs the NCA pivots (piv_in/piv_out)");
+      rin_rec[ch].resize(nc);
+      rout_rec[ch].resize(nc);
+      for (int io = 0; io < 2; ++io) {
+        const int64_t* ptr = io ? c.piv_out_ptr : c.piv_in_ptr;
+        const int64_t* idx = io ? c.piv_out : c.piv_in;
+        const int32_t* rank = io ? c.r_out : c.r_in;
+        auto& rec = io ? rout_rec[ch] : rin_rec[ch];
+        for (int64_t x = 0; x < nc; ++x) {
+          if (ptr[x + 1] - ptr[x] != rank[x])
+            return fail(H2G_ERR_BAD_EXPORT, "pivot count != rank");
+          rec[x] = (int64_t)s.recs.size();
+          for (int64_t k = ptr[x]; k < ptr[x + 1]; ++k) {
+            if (idx[k] < 0 || idx[k] >= N) return fail(H2G_ERR_BAD_EXPORT, "pivot out of range");
+            const Rec4 r = s.recs[idx[k]];
+            s.recs.push_back(r);
+          }
+        }
+      }
+    }
+  }
+  if ((int64_t)s.recs.size() >= (1LL << 31))
+    return fail(H2G_ERR_BAD_EXPORT, "too many point records for int32 indexing");
+  double share = d->m2l_recompute_share;
+  if (!(share > 0.0 && share < 1.0)) share = 1.0;
+
   // ================= part 0: before the exchange =================
   // ---- up_leaf: P2M of every channel ----
   begin_phase(s, PH_GEMV, "up_leaf");
@@ -569,16 +746,38 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
       emit_blr_reduce();
       reduce_pending = false;
     }
+    // hybrid split of the M2L targets (error diffusion over the level, by bytes)
+    double acc_all = 0.0, acc_rc = 0.0;
     for (int ch = 0; ch < d->n_channels; ++ch) {
       const h2g_channel_desc& c = d->channels[ch];
       for (int64_t x = lo[l]; x < lo[l + 1]; ++x) {
         const int64_t ri = c.r_in[x];
         if (ri == 0 || !mine(x, l)) continue;
+        bool must = false;
+        int64_t cols = 0;
         for (int64_t k = c.m2l_rowptr[x]; k < c.m2l_rowptr[x + 1]; ++k) {
           const int64_t y = c.m2l_src[k];
           if (y < 0 || y >= nc || level_of(y) != l)
             return fail(H2G_ERR_BAD_EXPORT, "m2l source not on the target's level");
           if (c.r_out[y] == 0) continue;
+          cols += c.r_out[y];
+          if (c.m2l_off[k] < 0) must = true;
+        }
+        bool rc = must;
+        if (!rc && need_m2l && (d->recompute & H2G_RECOMPUTE_M2L) && cols > 0) {
+          acc_all += (double)ri * cols;
+          if (acc_rc < share * acc_all) {
+            rc = true;
+            acc_rc += (double)ri * cols;
+          }
+        }
+        for (int64_t k = c.m2l_rowptr[x]; k < c.m2l_rowptr[x + 1]; ++k) {
+          const int64_t y = c.m2l_src[k];
+          if (c.r_out[y] == 0) continue;
+          if (rc) {
+            add_rc_term(s, rout_rec[ch][y], v_off[ch][y], c.r_out[y], false);
+            continue;
+          }
           if (!in_blob(d, c.m2l_off[k], ri, c.r_out[y]))
             return fail(H2G_ERR_BAD_EXPORT, "m2l out of blob");
           add_term(s, c.m2l_off[k], v_off[ch][y], ri, c.r_out[y]);
@@ -591,7 +790,7 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
             add_term(s, c.l2l_off[x], u_off[ch][px], ri, c.r_in[px]);
           }
         }
-        emit_task(s, u_off[ch][x], ri, bytes);
+        emit_task(s, u_off[ch][x], ri, bytes, rc ? rin_rec[ch][x] : -1);
       }
     }
     s.phases.back().alg_bytes = bytes;
@@ -620,18 +819,25 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
                  d->blr_rank[k]);  // leaf-blocked U: rows of x are one n_x x p block
       if (l > 1) a = parent(a, l);
     }
+    bool any_rc = false;
     for (int64_t k = d->near_rowptr[x]; k < d->near_rowptr[x + 1]; ++k) {
       const int64_t y = d->near_src[k];
       if (y < 0 || y >= nc) return fail(H2G_ERR_BAD_EXPORT, "near source out of range");
+      if (d->near_off[k] < 0 || (d->recompute & H2G_RECOMPUTE_NEAR)) {
+        add_rc_term(s, st[y], p->q_tree + st[y], nsz(y), y == x);
+        any_rc = true;
+        continue;
+      }
       if (!in_blob(d, d->near_off[k], nx, nsz(y)))
         return fail(H2G_ERR_BAD_EXPORT, "near block out of blob");
       add_term(s, d->near_off[k], p->q_tree + st[y], nx, nsz(y));
     }
-    emit_task(s, p->phi_tree + st[x], nx, bytes);
+    emit_task(s, p->phi_tree + st[x], nx, bytes, any_rc ? st[x] : -1);
   }
   s.phases.back().alg_bytes = bytes;
   end_phase(s);
   split_heavy_tasks(s, p->n_slots, ones_off);
+  partition_engines(s);
   return H2G_OK;
 }
 
@@ -649,7 +855,9 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
                   std::vector<int64_t>& cta, int kb = 1, bool mma = false) {
   for (Phase& ph : phases) {
     if (ph.kind != PH_GEMV) continue;
-    const int64_t nt = ph.task_end - ph.task_begin;
+    const int64_t nt = stream_end_of(ph) - ph.task_begin;
+    // hybrid phases share the SMs with the P2P engine: one streaming CTA per SM
+    const int n_cta_ph = ph.hybrid ? std::max(1, n_cta / kCtasPerSm) : n_cta;
     std::vector<HostChunk> pc;  // this phase's chunks in task order
     std::vector<int64_t> task_chunk0(nt + 1);
     std::vector<double> task_cost(nt);
@@ -732,7 +940,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
     }
     task_chunk0[nt] = (int64_t)pc.size();
     // partition tasks over CTAs by cost
-    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(nt, n_cta));
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(nt, n_cta_ph));
     std::vector<int64_t> cut_at(1, 0);
     double acc = 0;
     for (int64_t ti = 0; ti < nt; ++ti) {
@@ -748,7 +956,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
     // narrow phase (fewer tasks than consumer warps on the GPU): split mode
     // (single RHS only; the batched engine always runs owned tasks)
     // (the tensor-pipe batched engine shares every chunk among the warps)
-    ph.split = (mma || (kb == 1 && nt < (int64_t)kConsumers * n_cta)) ? 1 : 0;
+    ph.split = (mma || (kb == 1 && nt < (int64_t)kConsumers * n_cta_ph)) ? 1 : 0;
     // per CTA: tasks -> warps (greedy by cost), interleave queues
     ph.cta_off = (int64_t)cta.size();
     for (size_t g = 0; g + 1 < cut_at.size(); ++g) {
@@ -863,21 +1071,66 @@ inline int grid_for(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 8));
 }
 
-int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s) {
+int launch_p2p(h2g_plan* p, const Phase& ph, int phase_idx, cudaStream_t s) {
+  const int64_t b = stream_end_of(ph), n = ph.task_end - b;
+  if (n <= 0) return H2G_OK;
+  // one CTA per task; in hybrid phases half the P2P CTAs per SM (beside the
+  // streaming CTA)
+  const int64_t per_sm = ph.hybrid ? std::max(1, kP2PCtasPerSm / 2) : kP2PCtasPerSm;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, p->n_sm * per_sm));
+  const P2PTask* tk = p->d_p2p_tasks + ph.p2p_off;
+  int* ctr = p->d_ctr + 2 * phase_idx;
+  const int kt = p->kernel_type, d3 = p->dim >= 3;
+#define H2G_LAUNCH_P2P(KT, DIM)                                                        \
+  p2p_tasks_kernel<KT, DIM><<<grid, kP2PThreads, 0, s>>>(                              \
+      tk, (int)n, p->d_p2p_terms, p->d_p2p_chunks, p->d_recs4, p->d_blob, p->d_arena, \
+      p->kp, ctr)
+  if (kt == 0) {
+    if (d3) H2G_LAUNCH_P2P(0, 3); else H2G_LAUNCH_P2P(0, 2);
+  } else if (kt == 1) {
+    if (d3) H2G_LAUNCH_P2P(1, 3); else H2G_LAUNCH_P2P(1, 2);
+  } else {
+    if (d3) H2G_LAUNCH_P2P(2, 3); else H2G_LAUNCH_P2P(2, 2);
+  }
+#undef H2G_LAUNCH_P2P
+  CUDA_TRY(cudaGetLastError());
+  return H2G_OK;
+}
+
+int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s, int phase_idx = 0) {
   const int64_t n = ph.task_end - ph.task_begin;
   if (n <= 0) return H2G_OK;
-  if (ph.kind == PH_GEMV && p->engine == 1) {
-    if (ph.split)
-      stream_gemv_kernel<true><<<ph.n_cta, kStreamThreads, kStreamSmem, s>>>(
-          p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
-    else
-      stream_gemv_kernel<false><<<ph.n_cta, kStreamThreads, kStreamSmem, s>>>(
-          p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
-  } else {
-    gemv_tasks_kernel<<<(unsigned)n, kWarps * 32, 0, s>>>(p->d_tasks + ph.task_begin, p->d_terms,
-                                                          p->d_blob, p->d_arena);
+  const int64_t se = stream_end_of(ph);
+  const bool has_stream = se > ph.task_begin, has_p2p = ph.task_end > se;
+  const bool fork = has_stream && has_p2p && p->stream2;
+  if (fork) {  // P2P engine on a parallel branch, joined before the next phase
+    CUDA_TRY(cudaEventRecord(p->ev_fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
   }
-  CUDA_TRY(cudaGetLastError());
+  if (has_stream) {
+    if (ph.kind == PH_GEMV && p->engine == 1) {
+      // hybrid: a larger smem request pins one streaming CTA per SM
+      const size_t smem = ph.hybrid ? kStreamSmemHybrid : kStreamSmem;
+      if (ph.split)
+        stream_gemv_kernel<true><<<ph.n_cta, kStreamThreads, smem, s>>>(
+            p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
+      else
+        stream_gemv_kernel<false><<<ph.n_cta, kStreamThreads, smem, s>>>(
+            p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
+    } else {
+      gemv_tasks_kernel<<<(unsigned)(se - ph.task_begin), kWarps * 32, 0, s>>>(
+          p->d_tasks + ph.task_begin, p->d_terms, p->d_blob, p->d_arena);
+    }
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (has_p2p) {
+    int rc = launch_p2p(p, ph, phase_idx, fork ? p->stream2 : s);
+    if (rc) return rc;
+  }
+  if (fork) {
+    CUDA_TRY(cudaEventRecord(p->ev_join, p->stream2));
+    CUDA_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
+  }
   return H2G_OK;
 }
 
@@ -886,8 +1139,8 @@ int run_middle(h2g_plan* p, cudaStream_t s) {
     CUDA_TRY(cudaGraphLaunch(p->graph_exec, s));
     return H2G_OK;
   }
-  for (const Phase& ph : p->phases) {
-    int rc = launch_phase(p, ph, s);
+  for (size_t i = 0; i < p->phases.size(); ++i) {
+    int rc = launch_phase(p, p->phases[i], s, (int)i);
     if (rc) return rc;
   }
   return H2G_OK;
@@ -926,6 +1179,14 @@ void free_plan(h2g_plan* p) {
   cudaFree(p->d_hq);
   cudaFree(p->d_hphi);
   cudaFree(p->d_cta);
+  cudaFree(p->d_recs4);
+  cudaFree(p->d_p2p_tasks);
+  cudaFree(p->d_p2p_terms);
+  cudaFree(p->d_p2p_chunks);
+  cudaFree(p->d_ctr);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
+  if (p->stream2) cudaStreamDestroy(p->stream2);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -933,6 +1194,29 @@ void free_plan(h2g_plan* p) {
 // Shard ownership for (rank, nranks): L_s = the first level with >= 4
 // subtrees per rank (capped at kappa); rank r owns the Morton range
 // [r*S/R, (r+1)*S/R) of the S = 2^(d*L_s) subtrees.
+// Do two distinct points share coordinates?  (Then r == 0 can occur off the
+// diagonal and every evaluated entry needs the zero_value test.)
+bool has_coincident_points(const h2g_export_desc* d) {
+  const int64_t N = d->n_points;
+  const int dim = d->dim;
+  const double* x = d->points_tree;
+  std::vector<int64_t> idx(N);
+  for (int64_t i = 0; i < N; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+    for (int k = 0; k < dim; ++k) {
+      const double u = x[a * dim + k], v = x[b * dim + k];
+      if (u != v) return u < v;
+    }
+    return false;
+  });
+  for (int64_t i = 1; i < N; ++i) {
+    bool same = true;
+    for (int k = 0; k < dim && same; ++k) same = x[idx[i] * dim + k] == x[idx[i - 1] * dim + k];
+    if (same) return true;
+  }
+  return false;
+}
+
 Shard make_shard(const h2g_export_desc* d, int rank, int nranks) {
   Shard sh;
   sh.rank = rank;
@@ -1017,6 +1301,17 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
   }
   p->row_begin = p->shard.row_bound[rank];
   p->row_end = p->shard.row_bound[rank + 1];
+  for (const Phase& ph : s.phases)
+    if (stream_end_of(ph) < ph.task_end) p->has_p2p = true;
+  if (p->has_p2p) {
+    p->kernel_type = d->kernel_type;
+    p->dim = d->dim;
+    p->kp.zero_value = d->zero_value;
+    p->kp.self_value = (d->has_diag ? d->diag : d->zero_value) + d->shift;
+    p->kp.gauss_c = d->sigma > 0 ? -1.0 / (2.0 * d->sigma * d->sigma) : 0.0;
+    p->kp.check = has_coincident_points(d) ? 1 : 0;
+    p->use_batched = false;  // the tensor-pipe engine streams stored blocks only
+  }
   std::vector<double> local_blob;
   if (nranks > 1) compact_blob(d, s, local_blob);
   {
@@ -1037,6 +1332,7 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
   p->phases = s.phases;
   p->n_tasks = (int64_t)s.tasks.size();
   p->sched = s;
+  std::vector<Rec4>().swap(p->sched.recs);  // uploaded below; the batched build never needs them
   p->n_terms = (int64_t)s.terms.size();
   if (p->n_terms >= (1LL << 31)) {
     delete p;
@@ -1099,10 +1395,34 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     if ((r = upload((void**)&p->d_tasks, s.tasks.data(), sizeof(Task) * s.tasks.size()))) return r;
     if ((r = upload((void**)&p->d_terms, s.terms.data(), sizeof(Term) * s.terms.size()))) return r;
     if ((r = upload((void**)&p->d_cta, cta.data(), sizeof(int64_t) * cta.size()))) return r;
+    if (p->has_p2p) {
+      static_assert(sizeof(Rec4) == sizeof(double4), "record layout");
+      p->n_recs = (int64_t)s.recs.size();
+      if ((r = upload((void**)&p->d_recs4, s.recs.data(), sizeof(Rec4) * s.recs.size()))) return r;
+      std::vector<P2PTask> pt;
+      std::vector<Term> pterms;
+      std::vector<P2PChunk> pch;
+      build_p2p_lists(s, p->phases, pt, pterms, pch);
+      if ((int64_t)pch.size() >= (1LL << 31)) return fail(H2G_ERR_BAD_EXPORT, "too many chunks");
+      if ((r = upload((void**)&p->d_p2p_tasks, pt.data(), sizeof(P2PTask) * pt.size()))) return r;
+      if ((r = upload((void**)&p->d_p2p_terms, pterms.data(), sizeof(Term) * pterms.size())))
+        return r;
+      if ((r = upload((void**)&p->d_p2p_chunks, pch.data(), sizeof(P2PChunk) * pch.size())))
+        return r;
+      p->workspace_bytes += sizeof(P2PTask) * pt.size() + sizeof(Term) * pterms.size() +
+                            sizeof(P2PChunk) * pch.size();
+      CUDA_TRY(cudaMalloc((void**)&p->d_ctr, sizeof(int) * 2 * std::max<size_t>(1, p->phases.size())));
+      CUDA_TRY(cudaMemset(p->d_ctr, 0, sizeof(int) * 2 * std::max<size_t>(1, p->phases.size())));
+      CUDA_TRY(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    }
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kStreamSmemHybrid));
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kStreamSmemHybrid));
     CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<8>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem));
     CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<16>,
@@ -1120,7 +1440,8 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
       make_records(chunks, segs, p->d_blob, p->d_arena, recs);
       if ((r = upload((void**)&p->d_recs, recs.data(), sizeof(ChunkRec) * recs.size()))) return r;
     }
-    p->workspace_bytes = sizeof(double) * p->n_slots + sizeof(Task) * s.tasks.size() +
+    p->workspace_bytes += sizeof(double) * p->n_slots + sizeof(Task) * s.tasks.size() +
+                         sizeof(Rec4) * s.recs.size() +
                          sizeof(Term) * s.terms.size() +
                          sizeof(ChunkRec) * chunks.size() + sizeof(int64_t) * cta.size() +
                          sizeof(int32_t) * p->N;
@@ -1129,9 +1450,10 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     for (int part = 0; part < 2; ++part) {
       if (part == 1 && nranks == 1) break;
       CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-      for (const Phase& ph : p->phases) {
+      for (size_t pi = 0; pi < p->phases.size(); ++pi) {
+        const Phase& ph = p->phases[pi];
         if (nranks > 1 && ph.part != part) continue;
-        int lr = launch_phase(p, ph, p->stream);
+        int lr = launch_phase(p, ph, p->stream, (int)pi);
         if (lr) {
           cudaGraph_t g;
           cudaStreamEndCapture(p->stream, &g);
@@ -1188,6 +1510,8 @@ int ensure_batched(h2g_plan* p, int which) {
       sb.tasks.push_back(u);
     }
     q.task_end = (int64_t)sb.tasks.size();
+    q.stream_end = -1;
+    q.hybrid = 0;
     b.phases.push_back(q);
     b.red.push_back({r0, (int32_t)((int64_t)reds.size() - r0)});
   }
@@ -1425,7 +1749,12 @@ int h2g_launches_per_matvec(const h2g_plan* p, int64_t nrhs) {
     }
     return total;
   }
-  return (int)((p->phases.size() + 2) * (nrhs < 1 ? 1 : nrhs));
+  int per = 2;  // gather + scatter
+  for (const Phase& ph : p->phases) {
+    const int64_t se = stream_end_of(ph);
+    per += (se > ph.task_begin) + (ph.task_end > se);
+  }
+  return per * (int)(nrhs < 1 ? 1 : nrhs);
 }
 
 int h2g_matvec(h2g_plan* plan, const double* q_dev, double* phi_dev, int64_t n, int64_t nrhs,
@@ -1614,7 +1943,7 @@ int h2g_profile_phases(h2g_plan* p, const double* q_dev, double* phi_dev, int it
                                                        p->N);
     CUDA_TRY(cudaEventRecord(ev[1], s));
     for (size_t i = 0; i < p->phases.size(); ++i) {
-      int rc = launch_phase(p, p->phases[i], s);
+      int rc = launch_phase(p, p->phases[i], s, (int)i);
       if (rc) return rc;
       CUDA_TRY(cudaEventRecord(ev[2 + i], s));
     }

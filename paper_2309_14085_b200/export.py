@@ -65,7 +65,12 @@ def tree_layout(tree):
     return perm, lo, cl_start, cl_end
 
 
-def export_channel(tree, ops, blob: BlobWriter) -> PackedChannel:
+def export_channel(tree, ops, blob: BlobWriter, inv_perm=None) -> PackedChannel:
+    """One NestedOperatorSet (engine.py:117-130).  With ``inv_perm`` (original
+    index -> tree position) the NCA pivots t_i / s_o of every cluster
+    (PivotQuad, lowrank.py:45-59) are exported too, as tree positions: the
+    M2L blocks are exactly K[t_i(X), s_o(Y)] (engine.py:176-179), so the
+    device can evaluate them instead of streaming them."""
     nc = len(tree.clusters)
     quads = ops.quads
     r_in = np.zeros(nc, np.int32)
@@ -102,10 +107,22 @@ def export_channel(tree, ops, blob: BlobWriter) -> PackedChannel:
             src.append(y)
             offs.append(blob.put(M))
         rowptr[X + 1] = len(src)
+    piv = {}
+    if inv_perm is not None:
+        for name, attr in (("in", "t_i"), ("out", "s_o")):
+            ptr = np.zeros(nc + 1, np.int64)
+            idx = []
+            for cid, q in enumerate(quads):
+                if q is not None and not q.empty:
+                    ids = np.asarray(getattr(q, attr), dtype=np.int64)
+                    idx.append(inv_perm[ids])
+                    ptr[cid + 1] = len(ids)
+            piv[f"piv_{name}_ptr"] = np.cumsum(ptr)
+            piv[f"piv_{name}"] = (np.concatenate(idx) if idx else np.zeros(0)).astype(np.int64)
     return PackedChannel(r_in=r_in, r_out=r_out, p2m_off=p2m_off, l2p_off=l2p_off,
                          m2m_off=m2m_off, l2l_off=l2l_off, m2l_rowptr=rowptr,
                          m2l_src=np.asarray(src, np.int32),
-                         m2l_off=np.asarray(offs, np.int64))
+                         m2l_off=np.asarray(offs, np.int64), **piv)
 
 
 def _put_leaf_blocked(blob: BlobWriter, U, tree, X: int) -> int:
@@ -139,7 +156,9 @@ def export_rep(rep, with_points: bool = True) -> PackedOperator:
     perm, lo, cl_start, cl_end = tree_layout(tree)
     nc = int(lo[-1])
     blob = BlobWriter()
-    channels = [export_channel(tree, ops, blob) for ops in rep.channels]
+    inv_perm = np.empty_like(perm)
+    inv_perm[perm] = np.arange(len(perm))
+    channels = [export_channel(tree, ops, blob, inv_perm) for ops in rep.channels]
 
     # BLR leg: factor dict is level-major / X asc / Y asc (blr.py:53-59);
     # rank-0 factors are skipped exactly as mvp_blr does (blr.py:79-80)

@@ -31,8 +31,13 @@ def _ptr(a: np.ndarray, ctype):
     return a.ctypes.data_as(C.POINTER(ctype))
 
 
-def _desc_from_packed(op: PackedOperator):
-    """Build the h2g_export_desc; returns (desc, keepalive list)."""
+def _desc_from_packed(op: PackedOperator, recompute: str = "", m2l_share: float = 1.0):
+    """Build the h2g_export_desc; returns (desc, keepalive list).
+
+    ``recompute``: comma list of block kinds evaluated from point
+    coordinates even where they are stored ("near", "m2l"); blocks exported
+    with offset -1 are always evaluated.  ``m2l_share`` in (0, 1): the share
+    of the M2L work evaluated while the rest streams concurrently."""
     keep = []
 
     def arr(a, dtype):
@@ -80,6 +85,33 @@ def _desc_from_packed(op: PackedOperator):
     blob = arr(op.blob, np.float64)
     d.blob_len = blob.size
     d.blob = _ptr(blob, C.c_double)
+    # kernel-evaluation path (ABI 3): points, kernel rules, pivots
+    for i, ch in enumerate(op.channels):
+        if ch.has_pivots:
+            cd = d.channels[i]
+            cd.piv_in_ptr = i64(ch.piv_in_ptr)
+            cd.piv_in = i64(ch.piv_in)
+            cd.piv_out_ptr = i64(ch.piv_out_ptr)
+            cd.piv_out = i64(ch.piv_out)
+    if op.points_tree is not None:
+        d.points_tree = _ptr(arr(op.points_tree, np.float64), C.c_double)
+    kern = op.kernel or {}
+    d.kernel_type = _lib.H2G_KERNELS.get(kern.get("name"), -1)
+    d.has_diag = kern.get("diag") is not None
+    d.zero_value = float(kern.get("zero_value", 0.0) or 0.0)
+    d.diag = float(kern.get("diag") or 0.0)
+    d.shift = float(kern.get("shift", 0.0) or 0.0)
+    d.sigma = float(kern.get("sigma") or 0.0)
+    mask = 0
+    for part in (recompute or "").replace(" ", "").split(","):
+        if part == "near":
+            mask |= _lib.H2G_RECOMPUTE_NEAR
+        elif part == "m2l":
+            mask |= _lib.H2G_RECOMPUTE_M2L
+        elif part:
+            raise ValueError(f"recompute: unknown block kind {part!r} (near, m2l)")
+    d.recompute = mask
+    d.m2l_recompute_share = float(m2l_share)
     return d, keep
 
 
@@ -94,10 +126,11 @@ def _torch():
 class GpuHierRep:
     """The operator of one reference ``HierRep``, resident on a B200."""
 
-    def __init__(self, op: PackedOperator, device: int = 0, lib=None):
+    def __init__(self, op: PackedOperator, device: int = 0, lib=None, recompute: str = "",
+                 m2l_share: float = 1.0):
         L = lib or _lib.load()
         op.validate()
-        desc, keep = _desc_from_packed(op)
+        desc, keep = _desc_from_packed(op, recompute, m2l_share)
         plan = C.c_void_p()
         _lib.check(L.h2g_plan_create(C.byref(desc), int(device), C.byref(plan)),
                    "h2g_plan_create")

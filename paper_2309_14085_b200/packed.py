@@ -46,6 +46,8 @@ ALIGN = 1  # doubles: blocks are packed back to back (TMA bulk copies align down
 
 CHANNEL_FIELDS = ("r_in", "r_out", "p2m_off", "l2p_off", "m2m_off", "l2l_off",
                   "m2l_rowptr", "m2l_src", "m2l_off")
+# NCA pivots (optional; the M2L kernel-evaluation path needs them)
+PIVOT_FIELDS = ("piv_in_ptr", "piv_in", "piv_out_ptr", "piv_out")
 
 
 @dataclass
@@ -58,7 +60,17 @@ class PackedChannel:
     l2l_off: np.ndarray    # int64[n_clusters]  r_in(c) x r_in(parent), keyed by child c
     m2l_rowptr: np.ndarray  # int64[n_clusters + 1]
     m2l_src: np.ndarray    # int32[nnz]
-    m2l_off: np.ndarray    # int64[nnz]  r_in(X) x r_out(Y)
+    m2l_off: np.ndarray    # int64[nnz]  r_in(X) x r_out(Y); -1 = evaluated, K[t_i(X), s_o(Y)]
+    # NCA pivots as TREE POSITIONS, CSR by cluster (PivotQuad.t_i / s_o,
+    # lowrank.py:45-59); None when not exported
+    piv_in_ptr: np.ndarray = None   # int64[n_clusters + 1]
+    piv_in: np.ndarray = None       # int64[sum r_in]
+    piv_out_ptr: np.ndarray = None  # int64[n_clusters + 1]
+    piv_out: np.ndarray = None      # int64[sum r_out]
+
+    @property
+    def has_pivots(self) -> bool:
+        return self.piv_in is not None and self.piv_out is not None
 
 
 @dataclass
@@ -83,7 +95,7 @@ class PackedOperator:
     blr_v_off: np.ndarray   # int64[nnz]
     near_rowptr: np.ndarray  # int64[n_clusters + 1]
     near_src: np.ndarray    # int32[nnz]
-    near_off: np.ndarray    # int64[nnz]
+    near_off: np.ndarray    # int64[nnz]; -1 = evaluated (store_near=False)
     blob: np.ndarray        # float64[blob_len]
     mem_scalars: int
     points_tree: np.ndarray = None  # float64[N, d] (optional; recompute paths)
@@ -178,6 +190,21 @@ class PackedOperator:
         del lo
         return int(tot)
 
+    def without_blocks(self, near: bool = True, m2l: bool = True) -> "PackedOperator":
+        """Shallow copy whose near and/or M2L blocks are marked "not stored"
+        (offset -1): the plan then evaluates them from points_tree / the
+        pivots, as the reference does with store_near=False
+        (engine.py:260-268).  The blob is shared, not compacted."""
+        import copy
+        op = copy.copy(self)
+        if near:
+            op.near_off = np.full_like(self.near_off, -1)
+        if m2l:
+            op.channels = [copy.copy(ch) for ch in self.channels]
+            for ch in op.channels:
+                ch.m2l_off = np.full_like(ch.m2l_off, -1)
+        return op
+
     # ------------------------------------------------------------- validate
     def validate(self):
         """Structural checks; raises ValueError("bad export: ...")."""
@@ -204,6 +231,17 @@ class PackedOperator:
                     bad(f"{f} length")
             if len(ch.m2l_src) != ch.m2l_rowptr[-1] or len(ch.m2l_off) != ch.m2l_rowptr[-1]:
                 bad("m2l nnz")
+            if ch.has_pivots:
+                if len(ch.piv_in_ptr) != nc + 1 or len(ch.piv_out_ptr) != nc + 1:
+                    bad("pivot CSR length")
+                if (not np.array_equal(np.diff(ch.piv_in_ptr), ch.r_in)
+                        or not np.array_equal(np.diff(ch.piv_out_ptr), ch.r_out)):
+                    bad("pivot count != rank")
+                for a in (ch.piv_in, ch.piv_out):
+                    if len(a) and (a.min() < 0 or a.max() >= self.N):
+                        bad("pivot out of range")
+        if self.points_tree is not None and self.points_tree.shape != (self.N, self.dim):
+            bad("points_tree shape")
         if len(self.near_src) != self.near_rowptr[-1]:
             bad("near nnz")
         if len(self.blr_src) != self.blr_rowptr[-1]:
@@ -235,6 +273,9 @@ class PackedOperator:
         for i, ch in enumerate(self.channels):
             for f in CHANNEL_FIELDS:
                 out[f"ch{i}_{f}"] = getattr(ch, f)
+            if ch.has_pivots:
+                for f in PIVOT_FIELDS:
+                    out[f"ch{i}_{f}"] = getattr(ch, f)
         if self.points_tree is not None:
             out["points_tree"] = self.points_tree
         return out
@@ -248,7 +289,9 @@ class PackedOperator:
             raise ValueError(f"bad export: schema {z['schema']!r} != {SCHEMA}")
         N, dim, kappa, n_max, mem, nch = (int(x) for x in z["scalars"])
         zv, dg, sh, sg = (float(x) for x in z["kernel_params"])
-        chans = [PackedChannel(**{f: np.asarray(z[f"ch{i}_{f}"]) for f in CHANNEL_FIELDS})
+        chans = [PackedChannel(**{f: np.asarray(z[f"ch{i}_{f}"]) for f in CHANNEL_FIELDS},
+                               **{f: np.asarray(z[f"ch{i}_{f}"]) for f in PIVOT_FIELDS
+                                  if f"ch{i}_{f}" in z})
                  for i in range(nch)]
         pts = np.asarray(z["points_tree"]) if "points_tree" in z else None
         return cls(variant=str(z["variant"]),

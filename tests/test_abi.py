@@ -51,10 +51,35 @@ def test_bad_descriptor_rejected_without_gpu():
         _lib.check(rc)
 
 
-def test_struct_layout_matches_header():
-    # 4 int32 + 3 int64 + 4 pointers + 2 channel descs (9 pointers each) + 8 ptrs + len + ptr
-    assert C.sizeof(_lib.ChannelDesc) == 9 * 8
-    assert C.sizeof(_lib.ExportDesc) == 16 + 24 + 32 + 2 * 72 + 8 * 8 + 8 + 8
+def _c_layout(struct, fields):
+    """sizeof / offsetof of a struct in include/h2g.h, from the C compiler."""
+    import subprocess
+    import tempfile
+    hdr = os.path.join(ROOT, "include", "h2g.h")
+    body = "".join(f'printf("%zu\\n", offsetof({struct}, {f}));' for f in fields)
+    src = (f'#include <stdio.h>\n#include <stddef.h>\n#include "{hdr}"\n'
+           f'int main(void) {{ printf("%zu\\n", sizeof({struct})); {body} return 0; }}\n')
+    with tempfile.TemporaryDirectory() as td:
+        c = os.path.join(td, "layout.c")
+        exe = os.path.join(td, "layout")
+        with open(c, "w") as fh:
+            fh.write(src)
+        subprocess.run(["gcc", "-o", exe, c], check=True)
+        out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.split()
+    return [int(x) for x in out]
+
+
+@pytest.mark.parametrize("ctype,cname", [("ChannelDesc", "h2g_channel_desc"),
+                                         ("ExportDesc", "h2g_export_desc"),
+                                         ("PlanStats", "h2g_plan_stats"),
+                                         ("ShardInfo", "h2g_shard_info")])
+def test_struct_layout_matches_header(ctype, cname):
+    """The ctypes mirrors in _lib.py have the C compiler's layout of h2g.h."""
+    cls = getattr(_lib, ctype)
+    names = [f for f, _ in cls._fields_]
+    want = _c_layout(cname, names)
+    got = [C.sizeof(cls)] + [getattr(cls, f).offset for f in names]
+    assert got == want
 
 
 def test_length_mismatch_maps_to_value_error():

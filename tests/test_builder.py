@@ -48,6 +48,10 @@ def test_structure_and_ranks_match_reference(name):
     assert np.array_equal(nop.near_src, op.near_src)
     assert nop.mem_scalars == op.mem_scalars == meta["mem_scalars"]
     assert nop.stored_scalars() == nop.mem_scalars
+    # the exported NCA pivots (tree positions) are the reference's own
+    for a, b in zip(nop.channels, op.channels):
+        for f in ("piv_in_ptr", "piv_in", "piv_out_ptr", "piv_out"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
 
 
 @pytest.mark.parametrize("name", NAMES)
@@ -99,3 +103,22 @@ def test_jittered_grid_generator():
     centres = -1.0 + (np.floor((p + 1.0) / h) + 0.5) * h
     assert np.all(np.abs(p - centres) <= 0.5 * h + 1e-15)
     assert p.min() >= -1.0 and p.max() <= 1.0
+
+
+@pytest.mark.parametrize("store", ["near", "m2l", ""])
+def test_unstored_blocks_build(store):
+    """store= drops raw kernel blocks from the blob (offset -1, evaluated on the
+    device); mem_scalars still counts them (engine.py:315) and the operator
+    acts exactly like the fully stored one."""
+    name = "g3d_lap_h2star"
+    op, nop, z, meta = _native_for(name)
+    pts = np.empty_like(op.points_tree)
+    pts[op.perm] = op.points_tree
+    sop = build_variant(meta["variant"], pts, kernel=meta["kernel"], n_max=meta["n_max"],
+                        eps=meta["eps"], store=store)
+    assert sop.mem_scalars == nop.mem_scalars
+    assert (sop.near_off < 0).all() == ("near" not in store)
+    for ch in sop.channels:
+        assert (ch.m2l_off < 0).all() == ("m2l" not in store)
+    assert len(sop.blob) < len(nop.blob)
+    assert rel_err(packed_matvec(sop, z["q"]), packed_matvec(nop, z["q"])) <= 1e-14

@@ -51,3 +51,34 @@ def test_length_mismatch():
     op, z, _ = load_golden(NAMES[0])
     with pytest.raises(ValueError, match="vector length mismatch"):
         packed_matvec(op, np.zeros(op.N + 1))
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_oracle_evaluated_blocks_match_reference(name):
+    """Blocks marked "not stored" (offset -1) are evaluated from the points /
+    NCA pivots by the oracle's restatement of Kernel.block (kernels.py:36-57):
+    the result still matches the reference's matvec on its stored operator
+    (engine.py:176-179: M2L = K[t_i, s_o]; engine.py:260-268 lazy near)."""
+    op, z, meta = load_golden(name)
+    assert all(ch.has_pivots for ch in op.channels)
+    ev = op.without_blocks(near=True, m2l=True)
+    ev.validate()
+    assert rel_err(packed_matvec(ev, z["q"]), z["phi_ref"]) <= 1e-13
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_exported_pivots_reproduce_stored_m2l(name):
+    """The exported pivots are the reference's: K[t_i(X), s_o(Y)] evaluated
+    from them equals every stored M2L block (engine.py:176-179)."""
+    from oracle.packed_matvec import kernel_block
+    op, z, meta = load_golden(name)
+    worst = 0.0
+    for ch in op.channels:
+        for X in range(op.n_clusters):
+            for k in range(ch.m2l_rowptr[X], ch.m2l_rowptr[X + 1]):
+                Y = ch.m2l_src[k]
+                M = op.mat(ch.m2l_off[k], ch.r_in[X], ch.r_out[Y])
+                K = kernel_block(op, ch.piv_in[ch.piv_in_ptr[X]:ch.piv_in_ptr[X + 1]],
+                                 ch.piv_out[ch.piv_out_ptr[Y]:ch.piv_out_ptr[Y + 1]])
+                worst = max(worst, float(np.max(np.abs(M - K), initial=0.0)))
+    assert worst <= 1e-15
