@@ -139,9 +139,59 @@ def cpu_port_time(op, q, budget_s=15.0, max_steps=20):
     return float(np.mean(times)), len(times)
 
 
-def bench_variant(op, args, torch, dev, rank, world):
+def recompute_for(cfg, arg):
+    """Which raw kernel blocks the device evaluates instead of streaming
+    (csrc/h2g_p2p.cuh).  "auto": whichever the measurements say is faster --
+    1/r and the Gaussian evaluate near + M2L (1.25-1.3x faster than streaming
+    them, profiles/), log r streams (fp64 log costs ~3x the bytes)."""
+    if arg != "auto":
+        return "" if arg in ("none", "stream") else arg
+    return "" if cfg["kernel"] == "log2d" else "near,m2l"
+
+
+def dgemm_tflops(torch, dev):
+    """Measured fp64 tensor-pipe peak on this GPU (cuBLAS DGEMM 8192^3)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=f"cuda:{dev}")
+    b = torch.randn(n, n, dtype=torch.float64, device=f"cuda:{dev}")
+    for _ in range(2):
+        torch.matmul(a, b)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        torch.matmul(a, b)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    del a, b
+    return 2 * n ** 3 * 5 / (e0.elapsed_time(e1) * 1e-3) / 1e12
+
+
+def bench_multi_rhs(rep, op, torch, dev, k=16, iters=10):
+    """Batched-RHS engine (csrc/h2g_stream.cuh stream_mma_kernel, DMMA): one
+    operator pass per 16 right-hand sides; fp64 TFLOP/s = 2 S k / t."""
+    Q = torch.randn(op.N, k, dtype=torch.float64, device=f"cuda:{dev}")
+    for _ in range(2):
+        rep.matmat(Q)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        rep.matmat(Q)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / iters
+    peak = dgemm_tflops(torch, dev)
+    tf = 2 * op.mem_scalars * k / (ms * 1e-3) / 1e12
+    return {"nrhs": k, "ms_per_block": ms, "matvec_per_s": k * 1e3 / ms,
+            "fp64_tflops": tf, "dgemm_peak_tflops": peak, "tensor_frac": tf / peak,
+            "hbm_roofline_tflops": 0.25 * k * _peaks()[0] / 1e3,
+            "launches": rep.launches_per_matvec(k)}
+
+
+def bench_variant(op, args, torch, dev, rank, world, recompute=""):
     from paper_2309_14085_b200.gpu_rep import GpuHierRep
-    rep = GpuHierRep(op, device=dev)
+    rep = GpuHierRep(op, device=dev, recompute=recompute)
     N = op.N
     q = np.random.default_rng(43).standard_normal(N)
     qd = torch.from_numpy(q).to(f"cuda:{dev}")
@@ -186,6 +236,8 @@ def bench_variant(op, args, torch, dev, rank, world):
     e2e_s = (time.perf_counter() - t0) / args.steps
     res = {"rep": rep, "ms": ms, "prof": prof, "clk": clk.summary(), "e2e_s": e2e_s,
            "q": q, "phi": phi, "out": out}
+    if args.nrhs > 1 and not recompute:
+        res["multi_rhs"] = bench_multi_rhs(rep, op, torch, dev, k=args.nrhs)
     return res
 
 
@@ -237,6 +289,10 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--variants", default="h2star-bt,h2plusH-star")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--recompute", default="auto",
+                    help="raw kernel blocks evaluated on the device: auto|none|near|m2l|near,m2l")
+    ap.add_argument("--nrhs", type=int, default=16,
+                    help="also time the batched-RHS engine with this many right-hand sides")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
@@ -292,7 +348,8 @@ def main():
         if world > 1:
             r = bench_variant_sharded(op, args, torch, dev, rank, world)
         else:
-            r = bench_variant(op, args, torch, dev, rank, world)
+            r = bench_variant(op, args, torch, dev, rank, world,
+                              recompute=recompute_for(cfg, args.recompute))
         r["op"] = op
         r["build_s"] = tb
         results[v] = r
@@ -308,20 +365,26 @@ def main():
     if world == 1:
         # roofline: streaming GEMV kernel phases (algorithmic bytes / event time)
         gemv = [p for p in R["prof"] if p["phase"] not in ("gather", "scatter", "blr_reduce")]
+        rc = recompute_for(cfg, args.recompute)
         k_bytes = sum(p["bytes"] for p in gemv)
         k_ms = sum(p["ms"] for p in gemv)
         achieved = k_bytes / (k_ms * 1e-3) / 1e9
         dom = max(gemv, key=lambda p: p["ms"])
         dom = {"name": dom["phase"], "ms": dom["ms"],
                "GBps": dom["bytes"] / (dom["ms"] * 1e-3) / 1e9}
-        kernel = "stream_gemv_kernel (all GEMV phases)"
+        kernel = ("stream_gemv_kernel (all GEMV phases)" if not rc else
+                  f"stream_gemv_kernel + p2p_tasks_kernel (all phases; {rc} blocks evaluated "
+                  "on the fp64 pipe: achieved = stored-representation bytes / time, may "
+                  "exceed the HBM peak)")
     else:
         # per-GPU share of the algorithmic bytes over the whole (max-over-ranks) step
         achieved = alg_bytes / world / (R["ms"] * 1e-3) / 1e9
         dom = None
         kernel = "whole sharded matvec per GPU (all phases + NCCL all-gather)"
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{head}.json")
+    rc_used = recompute_for(cfg, args.recompute) if world == 1 else ""
+    tpath = os.path.join(ROOT, "profiles",
+                         f"traffic_{args.config}_{head}{'_eval' if rc_used else ''}.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
@@ -336,7 +399,8 @@ def main():
         "config": {"workload": cfg["desc"], "variant": head, "N": op.N, "kappa": op.kappa,
                    "mem_scalars": int(op.mem_scalars), "alg_bytes": alg_bytes,
                    "parallelism": f"subtree-sharded x{world}" if world > 1 else "single",
-                   "l2": "operator > L2 (no flush)", "build_s": round(R["build_s"], 2)},
+                   "l2": "operator > L2 (no flush)", "build_s": round(R["build_s"], 2),
+                   "evaluated_blocks": recompute_for(cfg, args.recompute) or "none"},
         "achieved_GBps": alg_bytes / (R["ms"] * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -349,6 +413,8 @@ def main():
     }
     if world > 1:
         line["shard"] = R["shard"]
+    if "multi_rhs" in R:
+        line["multi_rhs"] = R["multi_rhs"]
     others = {}
     for v in variants[1:]:
         r = results[v]

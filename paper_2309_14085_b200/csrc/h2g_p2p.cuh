@@ -245,8 +245,14 @@ __device__ __forceinline__ void p2p_task(const P2PTask& tk, const Term* __restri
   }
 }
 
-// rows-per-lane layout for m rows: L = clamp(pow2ceil(ceil(m / 4)), 4, 32),
-// J = ceil(m / L) (<= 8 since m <= kMaxRows = 256)
+// rows-per-lane layout for m rows: J ~ kP2PRowsPerLane independent row
+// chains per lane, L = clamp(pow2ceil(ceil(m / JT)), 4, 32) lanes per column
+// group, J = ceil(m / L) (<= 8 since m <= kMaxRows = 256)
+#ifndef H2G_P2P_JT
+#define H2G_P2P_JT 8
+#endif
+constexpr int kP2PRowsPerLane = H2G_P2P_JT;
+
 template <int KT, int DIM>
 __device__ __forceinline__ void p2p_dispatch(const P2PTask& tk, const Term* __restrict__ terms,
                                              const P2PChunk* __restrict__ chunks,
@@ -256,27 +262,34 @@ __device__ __forceinline__ void p2p_dispatch(const P2PTask& tk, const Term* __re
                                              double (*sx)[kP2PChunk], double* red, int lane,
                                              int warp) {
   const int m = tk.m;
-#define H2G_P2P(Lv, Jv)                                                                   \
+  constexpr int JT = kP2PRowsPerLane;
+  int L = 4;
+  while (L < 32 && L * JT < m) L <<= 1;
+  const int J = (m + L - 1) / L;
+#define H2G_P2P(Lv, Jv)                                                                     \
   p2p_task<KT, DIM, Lv, Jv>(tk, terms, chunks, recs, blob, arena, kp, srec, sx, red, lane, \
                             warp)
-  if (m <= 16) {
-    if (m <= 4) H2G_P2P(4, 1);
-    else if (m <= 8) H2G_P2P(4, 2);
-    else if (m <= 12) H2G_P2P(4, 3);
-    else H2G_P2P(4, 4);
-  } else if (m <= 32) {
-    if (m <= 24) H2G_P2P(8, 3);
-    else H2G_P2P(8, 4);
-  } else if (m <= 64) {
-    if (m <= 48) H2G_P2P(16, 3);
-    else H2G_P2P(16, 4);
-  } else {
-    if (m <= 96) H2G_P2P(32, 3);
-    else if (m <= 128) H2G_P2P(32, 4);
-    else if (m <= 160) H2G_P2P(32, 5);
-    else if (m <= 192) H2G_P2P(32, 6);
-    else H2G_P2P(32, 8);
+#define H2G_P2P_J(Lv)                                                  \
+  switch (J) {                                                         \
+    case 1: if constexpr (Lv == 4) { H2G_P2P(Lv, 1); } else { __trap(); } break;          \
+    case 2: if constexpr (Lv == 4) { H2G_P2P(Lv, 2); } else { __trap(); } break;          \
+    case 3: if constexpr (Lv == 4 || JT <= 4) { H2G_P2P(Lv, 3); } else { __trap(); } break; \
+    case 4: H2G_P2P(Lv, 4); break;                                     \
+    case 5: if constexpr (JT > 4 || Lv == 32) { H2G_P2P(Lv, 5); } else { __trap(); } break; \
+    case 6: if constexpr (JT > 4 || Lv == 32) { H2G_P2P(Lv, 6); } else { __trap(); } break; \
+    case 7: if constexpr (JT > 4 || Lv == 32) { H2G_P2P(Lv, 7); } else { __trap(); } break; \
+    default: if constexpr (JT > 4 || Lv == 32) { H2G_P2P(Lv, 8); } else { __trap(); } break; \
   }
+  if (L == 4) {
+    H2G_P2P_J(4)
+  } else if (L == 8) {
+    H2G_P2P_J(8)
+  } else if (L == 16) {
+    H2G_P2P_J(16)
+  } else {
+    H2G_P2P_J(32)
+  }
+#undef H2G_P2P_J
 #undef H2G_P2P
 }
 

@@ -1423,6 +1423,18 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kStreamSmemHybrid));
+    // P2P CTAs must not pin an SM to a small shared-memory carve-out: hybrid
+    // phases place a streaming CTA (> half the SM's smem) beside them
+#define H2G_P2P_CARVEOUT(KT, DIM)                                                       \
+  CUDA_TRY(cudaFuncSetAttribute(p2p_tasks_kernel<KT, DIM>,                              \
+                                cudaFuncAttributePreferredSharedMemoryCarveout, 100))
+    H2G_P2P_CARVEOUT(0, 2);
+    H2G_P2P_CARVEOUT(0, 3);
+    H2G_P2P_CARVEOUT(1, 2);
+    H2G_P2P_CARVEOUT(1, 3);
+    H2G_P2P_CARVEOUT(2, 2);
+    H2G_P2P_CARVEOUT(2, 3);
+#undef H2G_P2P_CARVEOUT
     CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<8>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem));
     CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<16>,
