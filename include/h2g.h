@@ -117,9 +117,10 @@ typedef struct h2g_export_desc {
   double sigma;               /* Gaussian width */
   int32_t recompute;          /* H2G_RECOMPUTE_* mask: evaluate these blocks even where stored */
   int32_t pad0;
-  double m2l_recompute_share; /* (0, 1]: share of the eligible M2L work (by bytes, per
-                                 level) evaluated on the fp64 pipe while the rest streams
-                                 concurrently from HBM; 0 or 1 = all of it */
+  double m2l_recompute_share; /* (0, 1]: with H2G_RECOMPUTE_M2L, the share of each level's
+                                 stored M2L entries evaluated; the rest of every target's
+                                 blocks stream through the same P2P task (fp64 pipe and HBM
+                                 busy at once); 0 or 1 = all of them */
 } h2g_export_desc;
 
 enum { H2G_KERNEL_LOG2D = 0, H2G_KERNEL_LAP3D = 1, H2G_KERNEL_GAUSSIAN = 2 };

@@ -67,9 +67,9 @@ struct Phase {
   int32_t n_cta = 0;
   int32_t split = 0;                     // 1: all warps per chunk (narrow phase)
   // tasks [task_begin, stream_end) run on the streaming engine, [stream_end,
-  // task_end) (tasks with kernel-evaluated terms) on the P2P engine
+  // task_end) on the P2P engine (a phase with kernel-evaluated terms runs
+  // wholly there)
   int64_t stream_end = -1;               // -1: all tasks stream
-  int32_t hybrid = 0;
   int64_t p2p_off = 0;                   // first P2PTask of the phase                    // both engines concurrently (1 stream CTA per SM)
 };
 
@@ -115,10 +115,6 @@ constexpr int64_t kSplitCtas = 4 * 296;       // pieces per phase: ~4 per persis
 constexpr int64_t kSplitMinBytes = 1 << 20;   // never cut below 1 MB pieces
 // batched-RHS engines: 8 or 16 right-hand sides per operator pass
 constexpr int kBatchKB[2] = {8, 16};
-// hybrid phases: a streaming CTA asks for more than half an SM's shared
-// memory, so exactly one lands per SM and a P2P CTA fits beside it
-constexpr size_t kStreamSmemHybrid = 118 * 1024;
-static_assert(kStreamSmemHybrid >= kStreamSmem, "hybrid smem below the engine's need");
 
 struct HostChunk {      // streaming chunk before decoding into a ChunkRec
   int64_t a_off;        // offset (doubles) of the first operator entry (blob or arena)
@@ -200,8 +196,6 @@ struct h2g_plan {
   int kernel_type = -1;
   int dim = 2;
   bool has_p2p = false;
-  cudaStream_t stream2 = nullptr;  // hybrid phases: the P2P engine's branch of the graph
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* d_hq = nullptr;    // host-call staging (h2g_matvec_host)
   double* d_hphi = nullptr;
   size_t h_cap = 0;
@@ -389,7 +383,6 @@ void split_heavy_tasks(HostSchedule& s, int64_t& slots, int64_t ones_off) {
     phases.push_back(main);
     if (!reduces.empty()) {
       Phase red = ph;
-      red.hybrid = 0;
       red.name = ph.name + "_red";
       red.alg_bytes = 0;
       red.task_begin = (int64_t)tasks.size();
@@ -403,23 +396,18 @@ void split_heavy_tasks(HostSchedule& s, int64_t& slots, int64_t ones_off) {
   s.phases.swap(phases);
 }
 
-// Inside every phase: streaming tasks first, then the P2P tasks (those with
-// kernel-evaluated terms) in decreasing cost order (the P2P engine fetches
-// them dynamically, largest first).
+// A phase with kernel-evaluated terms runs wholly on the P2P engine (its
+// stored terms through direct loads, overlapping the evaluation); its tasks
+// are put in decreasing cost order (fetched dynamically, largest first).
 void partition_engines(HostSchedule& s) {
   for (Phase& ph : s.phases) {
-    std::vector<Task> st_t, p2p_t;
-    std::vector<double> cost;
-    for (int64_t i = ph.task_begin; i < ph.task_end; ++i) {
-      const Task& t = s.tasks[i];
-      if (is_p2p_task(s, t)) p2p_t.push_back(t);
-      else st_t.push_back(t);
-    }
-    if (p2p_t.empty()) {
+    bool any = false;
+    for (int64_t i = ph.task_begin; i < ph.task_end && !any; ++i) any = is_p2p_task(s, s.tasks[i]);
+    if (!any) {
       ph.stream_end = -1;
-      ph.hybrid = 0;
       continue;
     }
+    std::vector<Task> st_t, p2p_t(s.tasks.begin() + ph.task_begin, s.tasks.begin() + ph.task_end);
     auto tcost = [&](const Task& t) {
       int64_t c = 0;
       for (int32_t k = t.t_begin; k < t.t_end; ++k) c += s.terms[k].ncols;
@@ -431,7 +419,6 @@ void partition_engines(HostSchedule& s) {
     for (const Task& t : st_t) s.tasks[i++] = t;
     ph.stream_end = i;
     for (const Task& t : p2p_t) s.tasks[i++] = t;
-    ph.hybrid = st_t.empty() ? 0 : 1;
   }
 }
 
@@ -746,36 +733,33 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
       emit_blr_reduce();
       reduce_pending = false;
     }
-    // hybrid split of the M2L targets (error diffusion over the level, by bytes)
+    // with share < 1, each target's M2L terms are split between evaluated and
+    // stored-and-streamed (error diffusion over the level, by entries): the
+    // P2P engine then keeps the fp64 pipe and HBM busy at once
     double acc_all = 0.0, acc_rc = 0.0;
     for (int ch = 0; ch < d->n_channels; ++ch) {
       const h2g_channel_desc& c = d->channels[ch];
       for (int64_t x = lo[l]; x < lo[l + 1]; ++x) {
         const int64_t ri = c.r_in[x];
         if (ri == 0 || !mine(x, l)) continue;
-        bool must = false;
-        int64_t cols = 0;
+        bool rc = false;  // some term of x evaluated
         for (int64_t k = c.m2l_rowptr[x]; k < c.m2l_rowptr[x + 1]; ++k) {
           const int64_t y = c.m2l_src[k];
           if (y < 0 || y >= nc || level_of(y) != l)
             return fail(H2G_ERR_BAD_EXPORT, "m2l source not on the target's level");
           if (c.r_out[y] == 0) continue;
-          cols += c.r_out[y];
-          if (c.m2l_off[k] < 0) must = true;
-        }
-        bool rc = must;
-        if (!rc && need_m2l && (d->recompute & H2G_RECOMPUTE_M2L) && cols > 0) {
-          acc_all += (double)ri * cols;
-          if (acc_rc < share * acc_all) {
-            rc = true;
-            acc_rc += (double)ri * cols;
+          bool ev = c.m2l_off[k] < 0;
+          if (!ev && (d->recompute & H2G_RECOMPUTE_M2L)) {
+            const double e = (double)ri * c.r_out[y];
+            acc_all += e;
+            if (acc_rc < share * acc_all) {
+              ev = true;
+              acc_rc += e;
+            }
           }
-        }
-        for (int64_t k = c.m2l_rowptr[x]; k < c.m2l_rowptr[x + 1]; ++k) {
-          const int64_t y = c.m2l_src[k];
-          if (c.r_out[y] == 0) continue;
-          if (rc) {
+          if (ev) {
             add_rc_term(s, rout_rec[ch][y], v_off[ch][y], c.r_out[y], false);
+            rc = true;
             continue;
           }
           if (!in_blob(d, c.m2l_off[k], ri, c.r_out[y]))
@@ -856,8 +840,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
   for (Phase& ph : phases) {
     if (ph.kind != PH_GEMV) continue;
     const int64_t nt = stream_end_of(ph) - ph.task_begin;
-    // hybrid phases share the SMs with the P2P engine: one streaming CTA per SM
-    const int n_cta_ph = ph.hybrid ? std::max(1, n_cta / kCtasPerSm) : n_cta;
+    const int n_cta_ph = n_cta;
     std::vector<HostChunk> pc;  // this phase's chunks in task order
     std::vector<int64_t> task_chunk0(nt + 1);
     std::vector<double> task_cost(nt);
@@ -1074,9 +1057,7 @@ inline int grid_for(int64_t n) {
 int launch_p2p(h2g_plan* p, const Phase& ph, int phase_idx, cudaStream_t s) {
   const int64_t b = stream_end_of(ph), n = ph.task_end - b;
   if (n <= 0) return H2G_OK;
-  // one CTA per task; in hybrid phases half the P2P CTAs per SM (beside the
-  // streaming CTA)
-  const int64_t per_sm = ph.hybrid ? std::max(1, kP2PCtasPerSm / 2) : kP2PCtasPerSm;
+  const int64_t per_sm = kP2PCtasPerSm;  // one CTA per task, persistent
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, p->n_sm * per_sm));
   const P2PTask* tk = p->d_p2p_tasks + ph.p2p_off;
   int* ctr = p->d_ctr + 2 * phase_idx;
@@ -1102,15 +1083,9 @@ int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s, int phase_idx = 0
   if (n <= 0) return H2G_OK;
   const int64_t se = stream_end_of(ph);
   const bool has_stream = se > ph.task_begin, has_p2p = ph.task_end > se;
-  const bool fork = has_stream && has_p2p && p->stream2;
-  if (fork) {  // P2P engine on a parallel branch, joined before the next phase
-    CUDA_TRY(cudaEventRecord(p->ev_fork, s));
-    CUDA_TRY(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
-  }
   if (has_stream) {
     if (ph.kind == PH_GEMV && p->engine == 1) {
-      // hybrid: a larger smem request pins one streaming CTA per SM
-      const size_t smem = ph.hybrid ? kStreamSmemHybrid : kStreamSmem;
+      const size_t smem = kStreamSmem;
       if (ph.split)
         stream_gemv_kernel<true><<<ph.n_cta, kStreamThreads, smem, s>>>(
             p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
@@ -1124,12 +1099,8 @@ int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s, int phase_idx = 0
     CUDA_TRY(cudaGetLastError());
   }
   if (has_p2p) {
-    int rc = launch_p2p(p, ph, phase_idx, fork ? p->stream2 : s);
+    int rc = launch_p2p(p, ph, phase_idx, s);
     if (rc) return rc;
-  }
-  if (fork) {
-    CUDA_TRY(cudaEventRecord(p->ev_join, p->stream2));
-    CUDA_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
   }
   return H2G_OK;
 }
@@ -1184,9 +1155,6 @@ void free_plan(h2g_plan* p) {
   cudaFree(p->d_p2p_terms);
   cudaFree(p->d_p2p_chunks);
   cudaFree(p->d_ctr);
-  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
-  if (p->ev_join) cudaEventDestroy(p->ev_join);
-  if (p->stream2) cudaStreamDestroy(p->stream2);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -1413,18 +1381,14 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
                             sizeof(P2PChunk) * pch.size();
       CUDA_TRY(cudaMalloc((void**)&p->d_ctr, sizeof(int) * 2 * std::max<size_t>(1, p->phases.size())));
       CUDA_TRY(cudaMemset(p->d_ctr, 0, sizeof(int) * 2 * std::max<size_t>(1, p->phases.size())));
-      CUDA_TRY(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
-      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
-      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
     }
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kStreamSmemHybrid));
+                                  (int)kStreamSmem));
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kStreamSmemHybrid));
-    // P2P CTAs must not pin an SM to a small shared-memory carve-out: hybrid
-    // phases place a streaming CTA (> half the SM's smem) beside them
+                                  (int)kStreamSmem));
+    // P2P kernels: maximum shared-memory carve-out (L1 is not what they need)
 #define H2G_P2P_CARVEOUT(KT, DIM)                                                       \
   CUDA_TRY(cudaFuncSetAttribute(p2p_tasks_kernel<KT, DIM>,                              \
                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100))
@@ -1523,7 +1487,6 @@ int ensure_batched(h2g_plan* p, int which) {
     }
     q.task_end = (int64_t)sb.tasks.size();
     q.stream_end = -1;
-    q.hybrid = 0;
     b.phases.push_back(q);
     b.red.push_back({r0, (int32_t)((int64_t)reds.size() - r0)});
   }
