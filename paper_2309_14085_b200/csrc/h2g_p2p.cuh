@@ -71,6 +71,17 @@ struct P2PChunk {      // 16 bytes: <= 32 columns of one evaluated block
   int32_t n_self;      // columns | kSelfBit (row and column runs share points)
 };
 
+// Bulk prefetch of [p, p + bytes) into L2 (TMA engine, no registers / smem).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint64_t bytes) {
+  const uint64_t a = reinterpret_cast<uint64_t>(p) & ~uint64_t(15);
+  uint64_t n = (reinterpret_cast<uint64_t>(p) + bytes + 15 - a) & ~uint64_t(15);
+  while (n > 0) {
+    const uint32_t b = (uint32_t)(n < (1u << 20) ? n : (1u << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + (n - b)), "r"(b) : "memory");
+    n -= b;
+  }
+}
+
 __device__ __forceinline__ double rsqrt_approx(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -134,23 +145,14 @@ __device__ __forceinline__ void p2p_task(const P2PTask& tk, const Term* __restri
     pz[j] = p.z;
     acc[j] = 0.0;
   }
-  // ---- stored terms (L2L, L2P, BLR U, stored blocks): columns dealt over
-  // (warp, lane group) pairs, direct coalesced loads down each column
-  for (int t = tk.t_begin; t < tk.t_end; ++t) {
-    const Term tm = terms[t];
-    const double* A = (tm.a_space ? arena : blob) + tm.a_off;
-    const double* x = arena + tm.x_off;
-#pragma unroll 2
-    for (int c = warp * G + g; c < tm.ncols; c += kP2PWarps * G) {
-      const double xv = x[c];
-      const double* col = A + (int64_t)c * tm.lda;
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        const int r = rl + L * j;
-        if (r < m) acc[j] = fma(ld_stream(col + r), xv, acc[j]);
-      }
+  // stored terms are read after the evaluation: start pulling them into L2 now
+  if (warp == 0)
+    for (int t = tk.t_begin + lane; t < tk.t_end; t += 32) {
+      const Term tm = terms[t];
+      if (tm.ncols > 0)
+        prefetch_l2((tm.a_space ? arena : blob) + tm.a_off,
+                    8ull * ((uint64_t)(tm.ncols - 1) * tm.lda + m));
     }
-  }
   // ---- evaluated chunks k = k_begin + warp, + kP2PWarps, ...: the next
   // chunk's records / x are loaded (registers) while the current one is
   // evaluated from the warp's smem buffer
@@ -221,6 +223,23 @@ __device__ __forceinline__ void p2p_task(const P2PTask& tk, const Term* __restri
       }
     }
     buf ^= 1;
+  }
+  // ---- stored terms (L2L, L2P, BLR U, stored blocks): columns dealt over
+  // (warp, lane group) pairs, direct coalesced loads down each column
+  for (int t = tk.t_begin; t < tk.t_end; ++t) {
+    const Term tm = terms[t];
+    const double* A = (tm.a_space ? arena : blob) + tm.a_off;
+    const double* x = arena + tm.x_off;
+#pragma unroll 2
+    for (int c = warp * G + g; c < tm.ncols; c += kP2PWarps * G) {
+      const double xv = x[c];
+      const double* col = A + (int64_t)c * tm.lda;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int r = rl + L * j;
+        if (r < m) acc[j] = fma(ld_stream(col + r), xv, acc[j]);
+      }
+    }
   }
   // ---- combine: lane groups by a fixed xor tree, then the warps in warp
   // order through smem; one store per row
@@ -307,6 +326,8 @@ p2p_tasks_kernel(const P2PTask* __restrict__ tasks, int n_tasks, const Term* __r
   __shared__ double red[kP2PWarps * kMaxRows];
   __shared__ int s_task;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  griddep_launch_dependents();
+  griddep_wait();  // x (and the counters' reset) come from earlier phases
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(ctr, 1);
     __syncthreads();

@@ -33,8 +33,8 @@
 
 #include "../../include/h2g.h"
 #include "h2g_kernels.cuh"
-#include "h2g_p2p.cuh"
 #include "h2g_stream.cuh"
+#include "h2g_p2p.cuh"
 
 using namespace h2g;
 
@@ -196,6 +196,7 @@ struct h2g_plan {
   int kernel_type = -1;
   int dim = 2;
   bool has_p2p = false;
+  bool pdl = true;  // phases launched with programmatic dependent launch (H2G_PDL=0: off)
   double* d_hq = nullptr;    // host-call staging (h2g_matvec_host)
   double* d_hphi = nullptr;
   size_t h_cap = 0;
@@ -1035,6 +1036,7 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
     }
     r.n_copies = nc;
     r.bytes_a = total;
+    if (c.a_space && c.ncols > 0) r.flags |= kArenaA;
     if (kb > 1) {  // X (ncols x kb) staged after the operator data, 16-byte aligned
       int64_t ext = strided_ext;
       for (int k = 0; k < nc; ++k)
@@ -1054,6 +1056,25 @@ inline int grid_for(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 8));
 }
 
+// Kernel launch, optionally with programmatic stream serialization (PDL):
+// the grid may launch while the previous kernel on the stream drains; the
+// kernels order their dependent reads with griddepcontrol.wait.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                     cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 int launch_p2p(h2g_plan* p, const Phase& ph, int phase_idx, cudaStream_t s) {
   const int64_t b = stream_end_of(ph), n = ph.task_end - b;
   if (n <= 0) return H2G_OK;
@@ -1062,10 +1083,10 @@ int launch_p2p(h2g_plan* p, const Phase& ph, int phase_idx, cudaStream_t s) {
   const P2PTask* tk = p->d_p2p_tasks + ph.p2p_off;
   int* ctr = p->d_ctr + 2 * phase_idx;
   const int kt = p->kernel_type, d3 = p->dim >= 3;
-#define H2G_LAUNCH_P2P(KT, DIM)                                                        \
-  p2p_tasks_kernel<KT, DIM><<<grid, kP2PThreads, 0, s>>>(                              \
-      tk, (int)n, p->d_p2p_terms, p->d_p2p_chunks, p->d_recs4, p->d_blob, p->d_arena, \
-      p->kp, ctr)
+#define H2G_LAUNCH_P2P(KT, DIM)                                                              \
+  CUDA_TRY(launch_k(p->pdl, p2p_tasks_kernel<KT, DIM>, grid, kP2PThreads, 0, s, tk, (int)n,  \
+                    (const Term*)p->d_p2p_terms, (const P2PChunk*)p->d_p2p_chunks,             \
+                    (const double4*)p->d_recs4, (const double*)p->d_blob, p->d_arena, p->kp, ctr))
   if (kt == 0) {
     if (d3) H2G_LAUNCH_P2P(0, 3); else H2G_LAUNCH_P2P(0, 2);
   } else if (kt == 1) {
@@ -1086,12 +1107,14 @@ int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s, int phase_idx = 0
   if (has_stream) {
     if (ph.kind == PH_GEMV && p->engine == 1) {
       const size_t smem = kStreamSmem;
+      const ChunkRec* recs = p->d_recs;
+      const int64_t* cta = p->d_cta + ph.cta_off;
       if (ph.split)
-        stream_gemv_kernel<true><<<ph.n_cta, kStreamThreads, smem, s>>>(
-            p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
+        CUDA_TRY(launch_k(p->pdl, stream_gemv_kernel<true>, (unsigned)ph.n_cta, kStreamThreads,
+                          smem, s, recs, cta, p->d_arena));
       else
-        stream_gemv_kernel<false><<<ph.n_cta, kStreamThreads, smem, s>>>(
-            p->d_recs, p->d_cta + ph.cta_off, p->d_arena);
+        CUDA_TRY(launch_k(p->pdl, stream_gemv_kernel<false>, (unsigned)ph.n_cta, kStreamThreads,
+                          smem, s, recs, cta, p->d_arena));
     } else {
       gemv_tasks_kernel<<<(unsigned)(se - ph.task_begin), kWarps * 32, 0, s>>>(
           p->d_tasks + ph.task_begin, p->d_terms, p->d_blob, p->d_arena);
@@ -1287,6 +1310,8 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     if (e && std::string(e) == "ldg") p->engine = 0;
     const char* b = getenv("H2G_BATCHED");
     if (b && std::string(b) == "0") p->use_batched = false;
+    const char* pd = getenv("H2G_PDL");
+    if (pd && std::string(pd) == "0") p->pdl = false;
     int nsm = 0;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess &&
         nsm > 0)

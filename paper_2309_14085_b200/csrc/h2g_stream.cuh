@@ -60,6 +60,8 @@ namespace h2g {
 #endif
 constexpr int kLastOfTask = 1;
 constexpr int kStridedRun = 2;                // record flag: one bulk copy per column
+constexpr int kArenaA = 4;                    // record flag: operator data lives in the arena
+                                              // (split-K partials written by the previous phase)
 constexpr int kConsumers = H2G_CONSUMERS;     // consumer warps per CTA
 constexpr int kStreamThreads = 32 * (1 + kConsumers);
 constexpr int kCtasPerSm = H2G_CTAS_PER_SM;   // independent pipelines per SM
@@ -109,6 +111,19 @@ constexpr size_t kStreamSmem = (size_t)kRing * 8 + (size_t)kConsumers * kXStrip 
                                (size_t)(2 * kSlots + kRecRing) * 8 + (size_t)kSlots * 4;
 
 // ---------------------------------------------------------------- PTX helpers
+// Programmatic dependent launch (phases launched with the programmatic
+// stream-serialization attribute): a phase's grid may start while the
+// previous one drains.  Everything a phase reads that the previous phase
+// wrote (coefficients in the arena) is read only after griddep_wait(); the
+// operator blob and the host-built records are read-only, so the producer
+// streams them ahead.  Without the attribute both are no-ops.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -596,6 +611,7 @@ stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict_
   const int64_t cb = cta_begin[blockIdx.x];
   const int n = (int)(cta_begin[blockIdx.x + 1] - cb);
   const ChunkRec* my = recs + cb;
+  griddep_launch_dependents();  // the next phase may start filling its rings
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSlots; ++s) {
@@ -615,6 +631,7 @@ stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict_
     int oldest = 0;        // oldest chunk not yet known to be released
     int head = 0;          // next free ring offset (doubles)
     int tail = 0;          // ring offset of chunk `oldest` (valid if oldest < i)
+    bool waited = false;   // griddep_wait() done (needed before arena-sourced copies)
     if (lane == 0)
       for (int j = 0; j < kRecAhead && j < n; ++j) {
         mbar_arrive_expect_tx(&recbar[j], sizeof(ChunkRec));
@@ -664,11 +681,16 @@ stream_gemv_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict_
         mbar_arrive_expect_tx(&full[s], h.bytes_a);
       }
       off = __shfl_sync(0xffffffffu, off, 0);
+      if ((h.flags & kArenaA) && !waited) {
+        griddep_wait();
+        waited = true;
+      }
       issue_operator_copies(h, reinterpret_cast<char*>(ring + off), &full[s], lane);
       __syncwarp();
     }
     return;
   }
+  griddep_wait();  // consumers read x (previous phases' outputs) from here on
 
   // ---------------------------------------------------- consumers
   const int cw = warp - 1;
