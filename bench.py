@@ -53,6 +53,17 @@ CONFIGS = {
                  desc="cfg2: 2D N=1048576 uniform [-1,1]^2, log r, leaf<=64, eps 1e-8"),
     "cfg3": dict(N=1048576, d=3, kernel="lap3d", n_max=64, eps=1e-6,
                  desc="cfg3: 3D N=1048576 uniform [-1,1]^3, 1/r, leaf<=64, eps 1e-6"),
+    # config 5's pipeline at 1/8 of its size: jittered 128^3 grid (cfg 5: 256^3,
+    # whose native build alone would take ~1.5 h of the box's 16 cores), only the
+    # transfer operators stored, near + M2L evaluated on the device
+    "cfg5s": dict(N=128 ** 3, d=3, kernel="lap3d", n_max=64, eps=1e-6, grid=128, store="",
+                  desc="cfg5 at 1/8 size: 3D jittered 128^3 grid in [-1,1]^3, 1/r, leaf<=64, "
+                       "eps 1e-6, near + M2L not stored (evaluated)"),
+    # config 4's kernel and shape at 1/16 of its size (the Gaussian at eps 1e-8 is
+    # near-dense: ranks ~1000 at N = 131,072, a 46 GB operator and a 36 min build)
+    "cfg4s": dict(N=32768, d=3, kernel="gaussian", n_max=64, eps=1e-8,
+                  desc="cfg4 at 1/16 size: 3D N=32768 uniform [-1,1]^3, Gaussian sigma 0.1 "
+                       "+ 1e-6 I, leaf<=64, eps 1e-8"),
 }
 # BASELINE.json "metric"; config.workload names the configuration measured
 METRIC = "H2* matvec/s and achieved HBM GB/s (fp64, 1/2/4/8 B200) vs ref CPU matvec"
@@ -120,10 +131,14 @@ def dist_env():
 
 
 def build_op(cfg, variant, n_threads=0):
-    from paper_2309_14085_b200.builder import build_variant, uniform_points
-    pts = uniform_points(cfg["N"], cfg["d"], 42)
+    from paper_2309_14085_b200.builder import build_variant, jittered_grid, uniform_points
+    if "grid" in cfg:
+        pts = jittered_grid(cfg["grid"], cfg["d"], 42)
+    else:
+        pts = uniform_points(cfg["N"], cfg["d"], 42)
     t0 = time.perf_counter()
-    op = build_variant(variant, pts, cfg["kernel"], cfg["n_max"], cfg["eps"], n_threads=n_threads)
+    op = build_variant(variant, pts, cfg["kernel"], cfg["n_max"], cfg["eps"], n_threads=n_threads,
+                       store=cfg.get("store", "near,m2l"))
     return op, time.perf_counter() - t0
 
 
@@ -139,14 +154,25 @@ def cpu_port_time(op, q, budget_s=15.0, max_steps=20):
     return float(np.mean(times)), len(times)
 
 
-def recompute_for(cfg, arg):
+def recompute_for(cfg, arg, op=None):
     """Which raw kernel blocks the device evaluates instead of streaming
-    (csrc/h2g_p2p.cuh).  "auto": whichever the measurements say is faster --
-    1/r and the Gaussian evaluate near + M2L (1.25-1.3x faster than streaming
-    them, profiles/), log r streams (fp64 log costs ~3x the bytes)."""
+    (csrc/h2g_p2p.cuh).  "auto": whichever the measurements say is faster
+    (DESIGN.md §3b) -- log r streams (the fp64 log costs ~3.5x the bytes);
+    1/r evaluates M2L (1.3x faster than streaming it) and the near field
+    only for leaves of >= 48 points on average (at ~32 points streaming the
+    near blocks is as fast); blocks the build did not store are always
+    evaluated."""
+    if cfg.get("store") == "":
+        return "near,m2l"
     if arg != "auto":
         return "" if arg in ("none", "stream") else arg
-    return "" if cfg["kernel"] == "log2d" else "near,m2l"
+    if cfg["kernel"] != "lap3d":
+        return ""
+    if op is not None:
+        n_leaves = int(op.level_offset[op.kappa + 1] - op.level_offset[op.kappa])
+        if op.N / max(1, n_leaves) >= 48:
+            return "near,m2l"
+    return "m2l"
 
 
 def dgemm_tflops(torch, dev):
@@ -187,6 +213,28 @@ def bench_multi_rhs(rep, op, torch, dev, k=16, iters=10):
             "fp64_tflops": tf, "dgemm_peak_tflops": peak, "tensor_frac": tf / peak,
             "hbm_roofline_tflops": 0.25 * k * _peaks()[0] / 1e3,
             "launches": rep.launches_per_matvec(k)}
+
+
+def bench_gmres(rep, op, torch, dev, k=16, restart=30, max_iter=300):
+    """Config 4's solve: restarted block GMRES(30) over k RHS ~ N(0,1)
+    (seed 43, reference bench.py:131-136), one batched operator application
+    per Arnoldi step (solver.py, CGS2), to relative residual 1e-8 or
+    max_iter steps; wall-clock on the host around the device-resident solve."""
+    from paper_2309_14085_b200.solver import gmres_block
+    B = torch.from_numpy(np.random.default_rng(43).standard_normal((k, op.N)).T.copy()).to(
+        f"cuda:{dev}")
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    X, r = gmres_block(rep.matmat, B, tol=1e-8, restart=restart, max_iter=max_iter,
+                       record_residuals=False)
+    torch.cuda.synchronize(dev)
+    t = time.perf_counter() - t0
+    R = B - rep.matmat(X)
+    true_res = float((torch.linalg.vector_norm(R, dim=0) / torch.linalg.vector_norm(B, dim=0)).max())
+    return {"nrhs": k, "restart": restart, "tol": 1e-8, "max_iter": max_iter, "seconds": t,
+            "arnoldi_steps": r.iterations, "operator_applications": r.matvecs,
+            "ms_per_step": t / max(1, r.iterations) * 1e3, "true_rel_residual_max": true_res,
+            "converged": bool(true_res <= 1e-8)}
 
 
 def bench_variant(op, args, torch, dev, rank, world, recompute=""):
@@ -238,6 +286,8 @@ def bench_variant(op, args, torch, dev, rank, world, recompute=""):
            "q": q, "phi": phi, "out": out}
     if args.nrhs > 1 and not recompute:
         res["multi_rhs"] = bench_multi_rhs(rep, op, torch, dev, k=args.nrhs)
+    if op.kernel.get("name") == "gaussian" and not recompute:
+        res["gmres"] = bench_gmres(rep, op, torch, dev, k=max(args.nrhs, 1))
     return res
 
 
@@ -349,7 +399,7 @@ def main():
             r = bench_variant_sharded(op, args, torch, dev, rank, world)
         else:
             r = bench_variant(op, args, torch, dev, rank, world,
-                              recompute=recompute_for(cfg, args.recompute))
+                              recompute=recompute_for(cfg, args.recompute, op))
         r["op"] = op
         r["build_s"] = tb
         results[v] = r
@@ -365,7 +415,7 @@ def main():
     if world == 1:
         # roofline: streaming GEMV kernel phases (algorithmic bytes / event time)
         gemv = [p for p in R["prof"] if p["phase"] not in ("gather", "scatter", "blr_reduce")]
-        rc = recompute_for(cfg, args.recompute)
+        rc = recompute_for(cfg, args.recompute, op)
         k_bytes = sum(p["bytes"] for p in gemv)
         k_ms = sum(p["ms"] for p in gemv)
         achieved = k_bytes / (k_ms * 1e-3) / 1e9
@@ -382,7 +432,7 @@ def main():
         dom = None
         kernel = "whole sharded matvec per GPU (all phases + NCCL all-gather)"
     traffic = None
-    rc_used = recompute_for(cfg, args.recompute) if world == 1 else ""
+    rc_used = recompute_for(cfg, args.recompute, op) if world == 1 else ""
     tpath = os.path.join(ROOT, "profiles",
                          f"traffic_{args.config}_{head}{'_eval' if rc_used else ''}.json")
     if os.path.exists(tpath):
@@ -400,7 +450,7 @@ def main():
                    "mem_scalars": int(op.mem_scalars), "alg_bytes": alg_bytes,
                    "parallelism": f"subtree-sharded x{world}" if world > 1 else "single",
                    "l2": "operator > L2 (no flush)", "build_s": round(R["build_s"], 2),
-                   "evaluated_blocks": recompute_for(cfg, args.recompute) or "none"},
+                   "evaluated_blocks": recompute_for(cfg, args.recompute, op) or "none"},
         "achieved_GBps": alg_bytes / (R["ms"] * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -415,6 +465,8 @@ def main():
         line["shard"] = R["shard"]
     if "multi_rhs" in R:
         line["multi_rhs"] = R["multi_rhs"]
+    if "gmres" in R:
+        line["gmres"] = R["gmres"]
     others = {}
     for v in variants[1:]:
         r = results[v]
@@ -424,7 +476,11 @@ def main():
                      "e2e_matvec_per_s": 1.0 / r["e2e_s"], "build_s": round(r["build_s"], 2)}
     if others:
         line["variants"] = others
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and cfg.get("store") == "":
+        line["cpu_baseline"] = {"value": None, "unit": "matvec/s", "cores": 1, "kind": "port",
+                                "sample": "not run: the operator's near/M2L blocks are not stored "
+                                          "and the numpy oracle would evaluate ~10^10 entries"}
+    elif rank == 0 and world == 1:
         t_cpu, n_cpu = cpu_port_time(op, R["q"], budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": 1.0 / t_cpu, "unit": "matvec/s", "cores": 1, "kind": "port",
                                 "sample": f"{n_cpu} full matvecs of the oracle port on the same "

@@ -131,30 +131,32 @@ __global__ void scatter_perm_kernel(const double* __restrict__ in,
     phi[(int64_t)perm[i] * ld] = in[i];
 }
 
-// batched RHS: out[i * KB + b] = q[perm[i] * ld + col0 + b] (0 for b >= nb)
+// Batched-RHS arena: KB / 8 planes of 8 doubles per slot; RHS b of slot s at
+// (b >> 3) * ps + 8 s + (b & 7) (h2g_stream.cuh, stream_mma_kernel).
+// batched RHS: q_tree (slot i of the planes at `out`) = q[perm[i] * ld + col0 + b]
 template <int KB>
 __global__ void gather_batch_kernel(const double* __restrict__ q, int64_t ld, int64_t col0,
                                     int nb, const int32_t* __restrict__ perm,
-                                    double* __restrict__ out, int64_t n) {
+                                    double* __restrict__ out, int64_t n, int64_t ps) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double* src = q + (int64_t)perm[i] * ld + col0;
 #pragma unroll
-    for (int b = 0; b < KB; ++b) out[i * KB + b] = b < nb ? src[b] : 0.0;
+    for (int b = 0; b < KB; ++b) out[(b >> 3) * ps + i * 8 + (b & 7)] = b < nb ? src[b] : 0.0;
   }
 }
 
-// batched RHS: phi[perm[i] * ld + col0 + b] = in[i * KB + b] for b < nb
+// batched RHS: phi[perm[i] * ld + col0 + b] = phi_tree (planes at `in`), b < nb
 template <int KB>
 __global__ void scatter_batch_kernel(const double* __restrict__ in,
                                      const int32_t* __restrict__ perm, double* __restrict__ phi,
-                                     int64_t ld, int64_t col0, int nb, int64_t n) {
+                                     int64_t ld, int64_t col0, int nb, int64_t n, int64_t ps) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double* dst = phi + (int64_t)perm[i] * ld + col0;
 #pragma unroll
     for (int b = 0; b < KB; ++b)
-      if (b < nb) dst[b] = in[i * KB + b];
+      if (b < nb) dst[b] = in[(b >> 3) * ps + i * 8 + (b & 7)];
   }
 }
 
@@ -183,15 +185,16 @@ struct RedTask {
 
 template <int KB>
 __global__ void reduce_partials_kernel(const RedTask* __restrict__ t, int n,
-                                       double* __restrict__ arena) {
+                                       double* __restrict__ arena, int64_t ps) {
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
     const RedTask r = t[k];
-    const int64_t len = (int64_t)r.m * KB;
-    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
-      const double* src = arena + r.part * KB + i;
+    const int64_t len = (int64_t)r.m * 8;  // per plane
+    for (int64_t i = threadIdx.x; i < len * (KB / 8); i += blockDim.x) {
+      const int64_t pl = i / len, ii = i - pl * len;
+      const double* src = arena + pl * ps + r.part * 8 + ii;
       double acc = 0.0;
       for (int p = 0; p < r.P; ++p) acc += src[(int64_t)p * len];
-      arena[r.y_off * KB + i] = acc;
+      arena[pl * ps + r.y_off * 8 + ii] = acc;
     }
   }
 }

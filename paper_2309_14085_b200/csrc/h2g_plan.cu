@@ -856,7 +856,8 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
       for (int32_t k = t.t_begin; k < t.t_end; ++k) {
         const Term& tm = s.terms[k];
         const bool strided = tm.lda != t.m;
-        const int64_t ldas = strided ? ((t.m + 1) & ~1) + 2 : t.m;
+        int64_t ldas = strided ? ((t.m + 1) & ~1) + 2 : t.m;
+        if (strided && kb > 1 && ldas % 16 == 0) ldas += 2;  // make_records: no 0 (mod 16)
         int64_t per = std::max<int64_t>(
             1, std::min<int64_t>(kChunkCols, mma ? kChunkAMma / (ldas + kb)
                                                  : kChunkA / std::max<int64_t>(ldas, 1)));
@@ -1012,6 +1013,9 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
         total += d.bytes;
       } else {  // strided run: one bulk copy per column, issued by the producer lanes
         r.ldas = ((c.m + 1) & ~1) + 2;
+        // batched engine: a smem column stride of 0 (mod 16) doubles would
+        // leave its A fragments 2-way bank-conflicted (h2g_stream.cuh mma_dd)
+        if (kb > 1 && r.ldas % 16 == 0) r.ldas += 2;
         r.a_shift = (int32_t)(c.a_off & 1);
         r.odd_lda = (c.lda & 1) ? 1 : 0;
         r.flags |= kStridedRun;
@@ -1029,7 +1033,7 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
       for (int k = 0; k < c.n_seg; ++k) {
         const Seg& sg = segs[c.seg_begin + k];
         r.seg_c0[k] = (int16_t)col;
-        r.seg_src[k] = arena + 8 * (uint64_t)sg.x_off * kb;
+        r.seg_src[k] = arena + 8 * (uint64_t)sg.x_off * (kb > 1 ? 8 : 1);  // plane 0
         col += sg.ncols;
       }
       r.seg_c0[c.n_seg] = (int16_t)col;
@@ -1480,6 +1484,10 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
   return H2G_OK;
 }
 
+// Plane stride (doubles) of the batched arenas: KB / 8 planes of 8 doubles
+// per slot (h2g_kernels.cuh)
+inline int64_t batch_plane(const h2g_plan* p) { return (p->n_slots + 8) * 8; }
+
 // Batched-RHS schedule (KB = kBatchKB[which]): the same tasks, cut into
 // chunks whose X (ncols x KB) also fits the ring, over an arena of KB-wide
 // slots; every chunk shared by the consumer warps of the tensor-pipe engine.
@@ -1534,6 +1542,7 @@ int ensure_batched(h2g_plan* p, int which) {
   if (!reds.empty())
     CUDA_TRY(cudaMemcpy(b.d_red, reds.data(), sizeof(RedTask) * reds.size(),
                         cudaMemcpyHostToDevice));
+  const int64_t ps = batch_plane(p);
   CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
   for (size_t k = 0; k < b.phases.size(); ++k) {
     const Phase& ph = b.phases[k];
@@ -1542,18 +1551,18 @@ int ensure_batched(h2g_plan* p, int which) {
       const int grid = std::min<int>(rr.second, 148 * 4);
       if (kb == 8)
         reduce_partials_kernel<8><<<grid, 256, 0, p->stream>>>(b.d_red + rr.first, rr.second,
-                                                               b.d_arena);
+                                                               b.d_arena, ps);
       else
         reduce_partials_kernel<16><<<grid, 256, 0, p->stream>>>(b.d_red + rr.first, rr.second,
-                                                                b.d_arena);
+                                                                b.d_arena, ps);
     }
     if (ph.task_end == ph.task_begin) continue;
     if (kb == 8)
       stream_mma_kernel<8><<<ph.n_cta, kMmaThreads, kMmaSmem, p->stream>>>(
-          b.d_recs, b.d_cta + ph.cta_off, b.d_arena);
+          b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps);
     else
       stream_mma_kernel<16><<<ph.n_cta, kMmaThreads, kMmaSmem, p->stream>>>(
-          b.d_recs, b.d_cta + ph.cta_off, b.d_arena);
+          b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps);
   }
   CUDA_TRY(cudaStreamEndCapture(p->stream, &b.graph));
   CUDA_TRY(cudaGraphInstantiate(&b.exec, b.graph, 0));
@@ -1588,20 +1597,21 @@ int matvec_impl(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nr
       if (rc) return rc;
       const h2g_plan::Batched& b = p->bat[which];
       const int nb = (int)std::min<int64_t>(kb, nrhs - c0);
+      const int64_t ps = batch_plane(p);
       if (kb == 8)
         gather_batch_kernel<8><<<grid_for(n), 256, 0, s>>>(
-            q, ld, c0, nb, p->d_perm, b.d_arena + (size_t)p->q_tree * kb, n);
+            q, ld, c0, nb, p->d_perm, b.d_arena + (size_t)p->q_tree * 8, n, ps);
       else
         gather_batch_kernel<16><<<grid_for(n), 256, 0, s>>>(
-            q, ld, c0, nb, p->d_perm, b.d_arena + (size_t)p->q_tree * kb, n);
+            q, ld, c0, nb, p->d_perm, b.d_arena + (size_t)p->q_tree * 8, n, ps);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaGraphLaunch(b.exec, s));
       if (kb == 8)
         scatter_batch_kernel<8><<<grid_for(n), 256, 0, s>>>(
-            b.d_arena + (size_t)p->phi_tree * kb, p->d_perm, phi, ld, c0, nb, n);
+            b.d_arena + (size_t)p->phi_tree * 8, p->d_perm, phi, ld, c0, nb, n, ps);
       else
         scatter_batch_kernel<16><<<grid_for(n), 256, 0, s>>>(
-            b.d_arena + (size_t)p->phi_tree * kb, p->d_perm, phi, ld, c0, nb, n);
+            b.d_arena + (size_t)p->phi_tree * 8, p->d_perm, phi, ld, c0, nb, n, ps);
       CUDA_TRY(cudaGetLastError());
       c0 += nb;
     }
