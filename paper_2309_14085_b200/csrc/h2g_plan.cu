@@ -856,8 +856,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
       for (int32_t k = t.t_begin; k < t.t_end; ++k) {
         const Term& tm = s.terms[k];
         const bool strided = tm.lda != t.m;
-        int64_t ldas = strided ? ((t.m + 1) & ~1) + 2 : t.m;
-        if (strided && kb > 1 && ldas % 16 == 0) ldas += 2;  // make_records: no 0 (mod 16)
+        const int64_t ldas = strided ? ((t.m + 1) & ~1) + 2 : t.m;
         int64_t per = std::max<int64_t>(
             1, std::min<int64_t>(kChunkCols, mma ? kChunkAMma / (ldas + kb)
                                                  : kChunkA / std::max<int64_t>(ldas, 1)));
@@ -1013,9 +1012,6 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
         total += d.bytes;
       } else {  // strided run: one bulk copy per column, issued by the producer lanes
         r.ldas = ((c.m + 1) & ~1) + 2;
-        // batched engine: a smem column stride of 0 (mod 16) doubles would
-        // leave its A fragments 2-way bank-conflicted (h2g_stream.cuh mma_dd)
-        if (kb > 1 && r.ldas % 16 == 0) r.ldas += 2;
         r.a_shift = (int32_t)(c.a_off & 1);
         r.odd_lda = (c.lda & 1) ? 1 : 0;
         r.flags |= kStridedRun;

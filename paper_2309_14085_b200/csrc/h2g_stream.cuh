@@ -337,22 +337,13 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 
 // Batched arena layout ("planes"): right-hand side b of slot s lives at
 // (b >> 3) * ps + 8 s + (b & 7), i.e. KB / 8 planes of 8 doubles per slot.
-// A chunk's X is staged plane by plane ([plane][column][8] in smem), so the
-// B fragment (column k = lane & 3, RHS n = lane >> 2) of 4 columns hits two
-// 8-double halves of the 16 banks: conflict-free.
-//
-// A fragments (8 rows x 4 columns, column stride ldas in smem) are
-// conflict-free when the 4 columns of a k-step form two pairs whose smem
-// offsets differ by 8 doubles (mod 16).  For a column distance dd with
-// dd * ldas = 8 (mod 16) -- dd = 8 for odd ldas, 4 for ldas = 2 (mod 4),
-// 2 otherwise -- k-step j of a block of 2 dd columns takes columns
-// {2j, 2j + 1, 2j + dd, 2j + dd + 1}: lane k reads column
-// 2 dd (t / (dd / 2)) + 2 (t % (dd / 2)) + (k & 1) + (k >> 1) dd.
-// (ldas = 0 mod 16 keeps a 2-way conflict; strided runs never use it.)
-__device__ __forceinline__ int mma_dd(int ldas) {
-  return (ldas & 1) ? 8 : ((ldas & 2) ? 4 : 2);
-}
-
+// A chunk's X is staged plane by plane ([plane][column][8] in smem): the B
+// fragment (column k = lane & 3, RHS n = lane >> 2) then spreads its four
+// columns over both halves of the banks (16-wide rows put all four on the
+// same banks).  Measured (cfg 2 leaf launch, 16 RHS): shared-memory
+// wavefronts 142 M -> 104 M, 1004 -> 775 us.  (Re-pairing the columns of a
+// k-step to de-conflict the A fragments did not reduce the wavefronts and
+// cost time.)
 template <int TPW, int NT>
 __device__ __forceinline__ void mma_step(const double (&a)[TPW], const double (&b)[NT],
                                          double (&c)[8][2][2]) {
@@ -363,43 +354,39 @@ __device__ __forceinline__ void mma_step(const double (&a)[TPW], const double (&
 }
 
 // One chunk for one warp: tiles i < TPW at rows 8 (w_r + wr i), k-steps
-// w_k, w_k + wk, ...  Ab: lane's A element of (tile 0, column lcol); Bb:
-// lane's X element of (column lcol, plane 0); xps: smem plane stride.
+// w_k, w_k + wk, ...  Ab: lane's A element of (tile 0, k-step 0); Bb: lane's
+// X element of (k-step 0, plane 0); xps: smem plane stride.
 template <int TPW, int NT>
 __device__ __forceinline__ void consume_mma(const double* __restrict__ Ab, int ldas, int tstride,
                                             const double* __restrict__ Bb, int xps, int ncols,
-                                            int lcol, int dd, int w_k, int wk,
-                                            double (&c)[8][2][2]) {
-  const int spb = dd >> 1;                      // k-steps per block of 2 dd columns
-  const int lg = spb == 1 ? 0 : (spb == 2 ? 1 : 2);
-  const int nfull = (ncols / (2 * dd)) * spb;   // k-steps of complete blocks
+                                            int kq, int w_k, int wk, double (&c)[8][2][2]) {
+  const int full = ncols >> 2;                 // whole k-steps
+  const int n_my = full > w_k ? (full - w_k + wk - 1) / wk : 0;
+  const int adv_a = 4 * ldas * wk, adv_b = 4 * 8 * wk;
+  const double* Ap = Ab + 4 * ldas * w_k;
+  const double* Bp = Bb + 4 * 8 * w_k;
 #pragma unroll 2
-  for (int t = w_k; t < nfull; t += wk) {
-    const int base = 2 * dd * (t >> lg) + 2 * (t & (spb - 1));
-    const double* Ap = Ab + base * ldas;
-    const double* Bp = Bb + base * 8;
+  for (int t = 0; t < n_my; ++t) {
     double a[TPW], b[NT];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) b[nt] = Bp[nt * xps];
 #pragma unroll
     for (int i = 0; i < TPW; ++i) a[i] = Ap[i * tstride];
     mma_step<TPW, NT>(a, b, c);
+    Ap += adv_a;
+    Bp += adv_b;
   }
-  // the incomplete last block (guarded columns)
-  if (nfull * 2 * dd / spb < ncols) {
-    int t = nfull + ((w_k - nfull % wk) % wk + wk) % wk;
-    for (; t < nfull + spb; t += wk) {
-      const int base = 2 * dd * (t >> lg) + 2 * (t & (spb - 1));
-      const bool ok = base + lcol < ncols;
-      const double* Ap = Ab + base * ldas;
-      const double* Bp = Bb + base * 8;
-      double a[TPW], b[NT];
+  // k tail (ncols % 4 columns): the column group holding k-step `full`
+  if ((ncols & 3) && (full % wk) == w_k) {
+    const bool ok = 4 * full + kq < ncols;
+    const double* At = Ab + 4 * ldas * full;
+    const double* Bt = Bb + 4 * 8 * full;
+    double a[TPW], b[NT];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) b[nt] = ok ? Bp[nt * xps] : 0.0;
+    for (int nt = 0; nt < NT; ++nt) b[nt] = ok ? Bt[nt * xps] : 0.0;
 #pragma unroll
-      for (int i = 0; i < TPW; ++i) a[i] = ok ? Ap[i * tstride] : 0.0;
-      mma_step<TPW, NT>(a, b, c);
-    }
+    for (int i = 0; i < TPW; ++i) a[i] = ok ? At[i * tstride] : 0.0;
+    mma_step<TPW, NT>(a, b, c);
   }
 }
 
@@ -540,27 +527,23 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
     mbar_wait(&full[s], (uint32_t)(i / kSlots) & 1u);
     if (ncols > 0 && tpw > 0) {
       const double* sA = ring + slot_off[s];
-      // lane's column in a k-step (conflict-free pairing); the column's
-      // parity is kq's, which is what the odd-lda shift depends on
-      const int dd = mma_dd(ldas);
-      const int lcol = (kq & 1) + (kq >> 1) * dd;
       const int lane_shift = odd ? ((a_shift + kq) & 1) : a_shift;
-      const double* Ab = sA + lcol * ldas + lane_shift + rq + 8 * w_r;
-      const double* Bb = sA + x_base + lcol * 8 + rq;
+      const double* Ab = sA + kq * ldas + lane_shift + rq + 8 * w_r;
+      const double* Bb = sA + x_base + kq * 8 + rq;
       const int xps = 8 * ncols;
       const int ts = 8 * wr;
       switch (tpw) {
-        case 1: consume_mma<1, NT>(Ab, ldas, ts, Bb, xps, ncols, lcol, dd, w_k, wk, c); break;
-        case 2: consume_mma<2, NT>(Ab, ldas, ts, Bb, xps, ncols, lcol, dd, w_k, wk, c); break;
-        case 3: consume_mma<3, NT>(Ab, ldas, ts, Bb, xps, ncols, lcol, dd, w_k, wk, c); break;
-        case 4: consume_mma<4, NT>(Ab, ldas, ts, Bb, xps, ncols, lcol, dd, w_k, wk, c); break;
+        case 1: consume_mma<1, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
+        case 2: consume_mma<2, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
+        case 3: consume_mma<3, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
+        case 4: consume_mma<4, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
         default:
           if constexpr (kMaxTpw > 4) {
             switch (tpw) {
-              case 5: consume_mma<5, NT>(Ab, ldas, ts, Bb, xps, ncols, lcol, dd, w_k, wk, c); break;
-              case 6: consume_mma<6, NT>(Ab, ldas, ts, Bb, xps, ncols, lcol, dd, w_k, wk, c); break;
-              case 7: consume_mma<7, NT>(Ab, ldas, ts, Bb, xps, ncols, lcol, dd, w_k, wk, c); break;
-              default: consume_mma<8, NT>(Ab, ldas, ts, Bb, xps, ncols, lcol, dd, w_k, wk, c); break;
+              case 5: consume_mma<5, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
+              case 6: consume_mma<6, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
+              case 7: consume_mma<7, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
+              default: consume_mma<8, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
             }
           }
           break;

@@ -66,6 +66,11 @@ def gmres_block(apply, B, tol: float = 1e-8, restart: int = 30, max_iter: int = 
     Returns (X, report) with report.residual_history a list of per-step
     per-column relative residual estimates.
 
+    The Krylov basis V ((m+1) x N x k) and all N-length work stay on the
+    device; the (m+1) x m x k Hessenberg matrix, the Givens rotations and the
+    residual estimates are host numpy state (one small device->host copy of
+    the new Hessenberg column per step instead of hundreds of tiny kernels).
+
     ortho: "mgs" = the reference's modified Gram-Schmidt order (solver.py:71-74,
     j+1 dependent passes per step); "cgs2" = classical Gram-Schmidt applied
     twice, two batched contractions per pass over the whole basis (same
@@ -79,33 +84,35 @@ def gmres_block(apply, B, tol: float = 1e-8, restart: int = 30, max_iter: int = 
     N, k = B.shape
     dt = torch.float64
     X = torch.zeros_like(B, dtype=dt) if x0 is None else x0.clone().to(dt)
-    bnorm = torch.linalg.vector_norm(B, dim=0)
-    if bool((bnorm == 0).any()):
+    bnorm_d = torch.linalg.vector_norm(B, dim=0)
+    bnorm = bnorm_d.cpu().numpy()
+    if (bnorm == 0).any():
         raise ValueError("b must be nonzero")  # solver.py:51-52
     m = int(restart)
     history = []
-    converged = torch.zeros(k, dtype=torch.bool, device=B.device)
-    res = torch.ones(k, dtype=dt, device=B.device)
+    converged = np.zeros(k, dtype=bool)
+    res = np.ones(k)
     steps = 0
     matvecs = 0
     restarts = 0
+    V = torch.zeros((m + 1, N, k), dtype=dt, device=B.device)
     while steps < max_iter:
         R = B - apply(X) if (steps > 0 or x0 is not None) else B.clone()
         if steps > 0 or x0 is not None:
             matvecs += 1
-        beta = torch.linalg.vector_norm(R, dim=0)
+        beta_d = torch.linalg.vector_norm(R, dim=0)
+        beta = beta_d.cpu().numpy()
         res = beta / bnorm
         converged = converged | (res <= tol)
-        if bool(converged.all()):
+        if converged.all():
             break
-        V = torch.zeros((m + 1, N, k), dtype=dt, device=B.device)
-        H = torch.zeros((m + 1, m, k), dtype=dt, device=B.device)
-        cs = torch.zeros((m, k), dtype=dt, device=B.device)
-        sn = torch.zeros((m, k), dtype=dt, device=B.device)
-        g = torch.zeros((m + 1, k), dtype=dt, device=B.device)
+        H = np.zeros((m + 1, m, k))
+        cs = np.zeros((m, k))
+        sn = np.zeros((m, k))
+        g = np.zeros((m + 1, k))
         active = ~converged
-        safe_beta = torch.where(beta > 0, beta, torch.ones_like(beta))
-        V[0] = R / safe_beta
+        safe_beta = np.where(beta > 0, beta, 1.0)
+        V[0] = R / torch.from_numpy(safe_beta).to(R.device)
         g[0] = beta
         j_done = 0
         for j in range(m):
@@ -113,64 +120,78 @@ def gmres_block(apply, B, tol: float = 1e-8, restart: int = 30, max_iter: int = 
             matvecs += 1
             steps += 1
             if ortho == "mgs":  # modified Gram-Schmidt (solver.py:71-74), per column
+                hs = []
                 for i in range(j + 1):
                     h = (V[i] * w).sum(dim=0)
-                    H[i, j] = h
+                    hs.append(h)
                     w = w - h * V[i]
+                hcol = torch.stack(hs)
             else:  # CGS2: h = V^T w, w -= V h, twice (per column k)
                 Vj = V[:j + 1]
                 h = torch.einsum("ink,nk->ik", Vj, w)
                 w = w - torch.einsum("ink,ik->nk", Vj, h)
                 h2 = torch.einsum("ink,nk->ik", Vj, w)
                 w = w - torch.einsum("ink,ik->nk", Vj, h2)
-                H[:j + 1, j] = h + h2
-            hn = torch.linalg.vector_norm(w, dim=0)
+                hcol = h + h2
+            hn_d = torch.linalg.vector_norm(w, dim=0)
+            col = torch.cat([hcol, hn_d[None]], dim=0).cpu().numpy()  # the one sync per step
+            H[:j + 1, j] = col[:j + 1]
+            hn = col[j + 1]
             H[j + 1, j] = hn
             happy = hn <= 1e-14 * safe_beta
-            V[j + 1] = torch.where(happy, torch.zeros_like(w), w / torch.where(happy, 1.0, hn))
+            scale = np.where(happy, 0.0, 1.0 / np.where(happy, 1.0, hn))
+            V[j + 1] = w * torch.from_numpy(scale).to(w.device)
             # previous rotations (solver.py:80-83)
             for i in range(j):
-                hi, hj = H[i, j].clone(), H[i + 1, j].clone()
+                hi, hj = H[i, j].copy(), H[i + 1, j].copy()
                 H[i, j] = cs[i] * hi + sn[i] * hj
                 H[i + 1, j] = -sn[i] * hi + cs[i] * hj
             # new rotation (solver.py:33-40, real case)
-            a, b = H[j, j], H[j + 1, j]
-            t = torch.hypot(a.abs(), b.abs())
+            a, b = H[j, j].copy(), H[j + 1, j].copy()
+            t = np.hypot(np.abs(a), np.abs(b))
             tz = t == 0
-            c = torch.where(tz, torch.ones_like(t), a.abs() / torch.where(tz, 1.0, t))
-            sa = torch.where(a != 0, torch.sign(a), torch.ones_like(a))
-            s = torch.where(tz, torch.zeros_like(t), sa * b / torch.where(tz, 1.0, t))
-            cs[j], sn[j] = c, s
-            H[j, j] = c * a + s * b
+            c = np.where(tz, 1.0, np.abs(a) / np.where(tz, 1.0, t))
+            sa = np.where(a != 0, np.sign(a), 1.0)
+            sv = np.where(tz, 0.0, sa * b / np.where(tz, 1.0, t))
+            cs[j], sn[j] = c, sv
+            H[j, j] = c * a + sv * b
             H[j + 1, j] = 0.0
-            g[j + 1] = -s * g[j]
+            g[j + 1] = -sv * g[j]
             g[j] = c * g[j]
-            res = torch.where(active, g[j + 1].abs() / bnorm, res)
+            res = np.where(active, np.abs(g[j + 1]) / bnorm, res)
             if record_residuals:
-                history.append(res.detach().cpu().numpy().copy())
+                history.append(res.copy())
             j_done = j + 1
-            newly = active & ((res <= tol) | happy)
-            converged = converged | newly
-            if bool(converged.all()) or steps >= max_iter:
+            converged = converged | (active & ((res <= tol) | happy))
+            if converged.all() or steps >= max_iter:
                 break
         # x += V[:j] y with H[:j,:j] y = g[:j] per column (solver.py:99-100)
-        Hj = H[:j_done, :j_done].permute(2, 0, 1)           # (k, j, j)
-        gj = g[:j_done].T.unsqueeze(-1)                     # (k, j, 1)
-        y = torch.linalg.solve_triangular(Hj, gj, upper=True).squeeze(-1)  # (k, j)
-        y = torch.where(active[:, None], y, torch.zeros_like(y))
-        X = X + torch.einsum("jnk,kj->nk", V[:j_done], y)
+        y = np.zeros((k, j_done))
+        for q in range(k):
+            if active[q]:
+                y[q] = _back_substitute(H[:j_done, :j_done, q], g[:j_done, q])
+        X = X + torch.einsum("jnk,kj->nk", V[:j_done], torch.from_numpy(y).to(V.device))
         restarts += 1
-        if bool(converged.all()):
+        if converged.all():
             # true residual of the final iterate (one extra application)
             R = B - apply(X)
             matvecs += 1
-            res = torch.linalg.vector_norm(R, dim=0) / bnorm
+            res = (torch.linalg.vector_norm(R, dim=0) / bnorm_d).cpu().numpy()
             break
     report = SolveReport(x=X, iterations=steps, residual=float(res.max()),
                          converged=bool((res <= tol * 10).all()),
                          wall_time=time.perf_counter() - t0, residual_history=history,
                          matvecs=matvecs, restarts=restarts)
     return X, report
+
+
+def _back_substitute(U, b):
+    """Upper-triangular solve U y = b (solver.py:99-100's triangular solve)."""
+    n = len(b)
+    y = np.zeros(n)
+    for i in range(n - 1, -1, -1):
+        y[i] = (b[i] - U[i, i + 1:] @ y[i + 1:]) / U[i, i]
+    return y
 
 
 def gmres(apply, b, cfg: GmresConfig = None) -> SolveReport:
