@@ -158,3 +158,21 @@ def test_split_k_pieces(monkeypatch, name):
             assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= TOL
     finally:
         rep.close()
+
+
+def test_pinned_host_calls_use_cached_graph(reps):
+    """Host-pointer calls on page-locked buffers replay one cached graph
+    (H2D + matvec + D2H); results equal the regular path, also after the
+    buffers change and after a multi-RHS call reallocates the staging."""
+    import torch
+    rep, op, z, meta = reps["g2d_log_h2star"]
+    q = torch.from_numpy(z["q"]).pin_memory().numpy()
+    out = torch.empty(op.N, dtype=torch.float64).pin_memory().numpy()
+    ref = rep.matvec(z["q"].copy())
+    for _ in range(3):
+        assert np.array_equal(rep.matvec(q, out=out), ref)
+    rep.matmat(z["Q"])  # grows the staging buffers
+    q2 = torch.from_numpy(2 * z["q"]).pin_memory().numpy()
+    out2 = torch.empty(op.N, dtype=torch.float64).pin_memory().numpy()
+    assert rel_err(rep.matvec(q2, out=out2), 2 * ref) <= 1e-15
+    assert np.array_equal(rep.matvec(q, out=out), ref)
