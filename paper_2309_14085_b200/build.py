@@ -24,7 +24,7 @@ NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
            "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 
 TARGETS = {
-    "libh2g.so": (["h2g_plan.cu"], ["h2g_kernels.cuh", "h2g_stream.cuh", "h2g_p2p.cuh"], "h2g.h"),
+    "libh2g.so": (["h2g_plan.cu"], ["h2g_kernels.cuh", "h2g_stream.cuh", "h2g_p2p.cuh", "h2g_eval.cuh"], "h2g.h"),
     "libh2b.so": (["h2b_build.cpp"], [], "h2b.h"),
 }
 CXX = os.environ.get("H2_CXX", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++")
