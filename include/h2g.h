@@ -165,6 +165,12 @@ int h2g_matvec_host(h2g_plan* plan, const double* q_host, double* phi_host, int6
 int h2g_profile_phases(h2g_plan* plan, const double* q_dev, double* phi_dev, int iters,
                        double* ms, int64_t* bytes, const char** names, int cap, int* n_out);
 
+/* Diagnostics: per-phase timing of one pass of the batched-RHS engine
+ * (kb = 8 or 16 right-hand sides; reduce + DMMA launches per phase).  Same
+ * output convention as h2g_profile_phases (bytes = stored operator bytes). */
+int h2g_profile_phases_batched(h2g_plan* plan, int kb, int iters, double* ms, int64_t* bytes,
+                               const char** names, int cap, int* n_out);
+
 /* Host-only: compile the schedule for `desc` as if for a device with n_sm
  * SMs (no CUDA calls) and write a JSON summary per phase into buf. */
 int h2g_schedule_info(const h2g_export_desc* desc, int n_sm, char* buf, int64_t buflen);

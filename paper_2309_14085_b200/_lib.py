@@ -60,7 +60,7 @@ class ShardInfo(C.Structure):
 
 # every symbol include/h2g.h declares (checked by tests/test_abi.py)
 H2G_SYMBOLS = ("h2g_plan_create", "h2g_plan_destroy", "h2g_plan_get_stats", "h2g_matvec",
-               "h2g_matvec_host", "h2g_profile_phases", "h2g_schedule_info",
+               "h2g_matvec_host", "h2g_profile_phases", "h2g_profile_phases_batched", "h2g_schedule_info",
                "h2g_launches_per_matvec",
                "h2g_error_string", "h2g_last_error_detail", "h2g_abi_version",
                "h2g_plan_create_sharded", "h2g_shard_get_info", "h2g_matvec_begin",
@@ -96,6 +96,8 @@ def load(path: str = None) -> C.CDLL:
     L.h2g_matvec_host.argtypes = [vp, P_F64, P_F64, C.c_int64, C.c_int64, C.c_int64]
     L.h2g_profile_phases.argtypes = [vp, vp, vp, C.c_int, P_F64, P_I64,
                                      C.POINTER(C.c_char_p), C.c_int, C.POINTER(C.c_int)]
+    L.h2g_profile_phases_batched.argtypes = [vp, C.c_int, C.c_int, P_F64, P_I64,
+                                             C.POINTER(C.c_char_p), C.c_int, C.POINTER(C.c_int)]
     L.h2g_launches_per_matvec.argtypes = [vp, C.c_int64]
     L.h2g_schedule_info.argtypes = [C.POINTER(ExportDesc), C.c_int, C.c_char_p, C.c_int64]
     L.h2g_plan_create_sharded.argtypes = [C.POINTER(ExportDesc), C.c_int, C.c_int, C.c_int,

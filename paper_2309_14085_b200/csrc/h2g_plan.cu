@@ -66,6 +66,7 @@ struct Phase {
   int64_t cta_off = 0;                   // streaming engine: CTA ranges at d_cta[cta_off ..]
   int32_t n_cta = 0;
   int32_t split = 0;                     // 1: all warps per chunk (narrow phase)
+  int32_t group = 0;                     // batched engine: warps per chunk stream (0: k-split)
   // tasks [task_begin, stream_end) run on the streaming engine, [stream_end,
   // task_end) on the P2P engine (a phase with kernel-evaluated terms runs
   // wholly there)
@@ -848,6 +849,21 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
     if (ph.kind != PH_GEMV) continue;
     const int64_t nt = stream_end_of(ph) - ph.task_begin;
     const int n_cta_ph = n_cta;
+    // Batched engine: a wide phase runs in GROUP mode -- G warps share a chunk
+    // stream, splitting only its rows (<= 8 tiles each), so tasks never need a
+    // cross-warp reduction: G = 1 (m <= 64), 2 (m <= 128), 4; kMmaConsumers / G
+    // interleaved streams per CTA, with smaller chunks (several in flight per
+    // stream).  Narrow phases keep the k-split sharing of every chunk.
+    ph.group = 0;
+    int64_t group_min_tasks = (int64_t)kMmaConsumers * n_cta_ph;
+    if (const char* e = getenv("H2G_MMA_GROUP_MIN_TASKS")) group_min_tasks = atoll(e);  // tests
+    if (mma && kMmaGroupMode && nt >= group_min_tasks) {
+      int mmax = 0;
+      for (int64_t ti = 0; ti < nt; ++ti) mmax = std::max(mmax, (int)s.tasks[ph.task_begin + ti].m);
+      ph.group = std::min(mmax <= 64 ? 1 : (mmax <= 128 ? 2 : 4), kMmaConsumers);
+    }
+    const int64_t chunk_mma =
+        ph.group > 0 ? std::min(kChunkAMmaGroup * ph.group, kChunkAMma) : kChunkAMma;
     std::vector<HostChunk> pc;  // this phase's chunks in task order
     std::vector<int64_t> task_chunk0(nt + 1);
     std::vector<double> task_cost(nt);
@@ -864,7 +880,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
         const bool strided = tm.lda != t.m;
         const int64_t ldas = strided ? ((t.m + 1) & ~1) + 2 : t.m;
         int64_t per = std::max<int64_t>(
-            1, std::min<int64_t>(kChunkCols, mma ? kChunkAMma / (ldas + kb)
+            1, std::min<int64_t>(kChunkCols, mma ? chunk_mma / (ldas + kb)
                                                  : kChunkA / std::max<int64_t>(ldas, 1)));
         if (strided) per = std::min<int64_t>(per, 32);  // one bulk copy per column (producer lane)
         if (mma) {  // whole 4-column k-steps, and enough of them per warp for tall tasks
@@ -947,6 +963,11 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
     // (single RHS only; the batched engine always runs owned tasks)
     // (the tensor-pipe batched engine shares every chunk among the warps)
     ph.split = (mma || (kb == 1 && nt < (int64_t)kConsumers * n_cta_ph)) ? 1 : 0;
+    int nq = kConsumers;  // interleaved queues per CTA (owned mode)
+    if (ph.group > 0) {
+      nq = kMmaConsumers / ph.group;
+      if (nq > 1) ph.split = 0;
+    }
     // per CTA: tasks -> warps (greedy by cost), interleave queues
     ph.cta_off = (int64_t)cta.size();
     for (size_t g = 0; g + 1 < cut_at.size(); ++g) {
@@ -956,19 +977,19 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
           chunks.push_back(pc[c]);
         continue;
       }
-      std::vector<int64_t> q[kConsumers];
-      double load[kConsumers] = {0};
+      std::vector<std::vector<int64_t>> q(nq);
+      std::vector<double> load(nq, 0.0);
       for (int64_t ti = cut_at[g]; ti < cut_at[g + 1]; ++ti) {
         int w = 0;
-        for (int v = 1; v < kConsumers; ++v)
+        for (int v = 1; v < nq; ++v)
           if (load[v] < load[w]) w = v;
         load[w] += task_cost[ti];
         for (int64_t c = task_chunk0[ti]; c < task_chunk0[ti + 1]; ++c) q[w].push_back(c);
       }
       size_t len = 0;
-      for (int w = 0; w < kConsumers; ++w) len = std::max(len, q[w].size());
+      for (int w = 0; w < nq; ++w) len = std::max(len, q[w].size());
       for (size_t r = 0; r < len; ++r)
-        for (int w = 0; w < kConsumers; ++w) {
+        for (int w = 0; w < nq; ++w) {
           if (r < q[w].size()) {
             chunks.push_back(pc[q[w][r]]);
           } else {
@@ -1573,10 +1594,10 @@ int ensure_batched(h2g_plan* p, int which) {
     if (ph.task_end == ph.task_begin) continue;
     if (kb == 8)
       stream_mma_kernel<8><<<ph.n_cta, kMmaThreads, kMmaSmem, p->stream>>>(
-          b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps);
+          b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps, ph.group);
     else
       stream_mma_kernel<16><<<ph.n_cta, kMmaThreads, kMmaSmem, p->stream>>>(
-          b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps);
+          b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps, ph.group);
   }
   CUDA_TRY(cudaStreamEndCapture(p->stream, &b.graph));
   CUDA_TRY(cudaGraphInstantiate(&b.exec, b.graph, 0));
@@ -1995,6 +2016,67 @@ int h2g_schedule_info(const h2g_export_desc* desc, int n_sm, char* buf, int64_t 
   out += "]}";
   if ((int64_t)out.size() + 1 > buflen) return fail(H2G_ERR_INVALID_ARG, "buffer too small");
   memcpy(buf, out.c_str(), out.size() + 1);
+  return H2G_OK;
+}
+
+// Batched-RHS engine, per phase: the reduce + DMMA launches of each phase of
+// one 8- or 16-wide pass (kb), timed with CUDA events on the plan stream over
+// the arena's current contents (timing does not depend on the values).
+int h2g_profile_phases_batched(h2g_plan* p, int kb, int iters, double* ms, int64_t* bytes,
+                               const char** names, int cap, int* n_out) {
+  if (!p || iters < 1 || (kb != 8 && kb != 16)) return fail(H2G_ERR_INVALID_ARG, "bad argument");
+  if (p->engine != 1 || p->has_p2p || p->shard.nranks > 1)
+    return fail(H2G_ERR_INVALID_ARG, "batched engine not available for this plan");
+  CUDA_TRY(cudaSetDevice(p->device));
+  const int which = kb == 8 ? 0 : 1;
+  int rc = ensure_batched(p, which);
+  if (rc) return rc;
+  const h2g_plan::Batched& b = p->bat[which];
+  const int64_t ps = batch_plane(p);
+  const int nph = (int)b.phases.size();
+  std::vector<cudaEvent_t> ev(nph + 1);
+  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+  std::vector<double> acc(nph, 0.0);
+  cudaStream_t s = p->stream;
+  CUDA_TRY(cudaDeviceSynchronize());
+  for (int it = 0; it < iters; ++it) {
+    CUDA_TRY(cudaEventRecord(ev[0], s));
+    for (int k = 0; k < nph; ++k) {
+      const Phase& ph = b.phases[k];
+      const auto& rr = b.red[k];
+      if (rr.second > 0) {
+        const int grid = std::min<int>(rr.second, 148 * 4);
+        if (kb == 8)
+          reduce_partials_kernel<8><<<grid, 256, 0, s>>>(b.d_red + rr.first, rr.second, b.d_arena, ps);
+        else
+          reduce_partials_kernel<16><<<grid, 256, 0, s>>>(b.d_red + rr.first, rr.second, b.d_arena, ps);
+      }
+      if (ph.task_end > ph.task_begin) {
+        if (kb == 8)
+          stream_mma_kernel<8><<<ph.n_cta, kMmaThreads, kMmaSmem, s>>>(b.d_recs, b.d_cta + ph.cta_off,
+                                                                       b.d_arena, ps, ph.group);
+        else
+          stream_mma_kernel<16><<<ph.n_cta, kMmaThreads, kMmaSmem, s>>>(b.d_recs, b.d_cta + ph.cta_off,
+                                                                        b.d_arena, ps, ph.group);
+      }
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaEventRecord(ev[k + 1], s));
+    }
+    CUDA_TRY(cudaEventSynchronize(ev[nph]));
+    for (int k = 0; k < nph; ++k) {
+      float t = 0;
+      CUDA_TRY(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
+      acc[k] += t;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  const int n = std::min(cap, nph);
+  for (int k = 0; k < n; ++k) {
+    ms[k] = acc[k] / iters;
+    bytes[k] = b.phases[k].alg_bytes;
+    names[k] = b.phases[k].name.c_str();
+  }
+  *n_out = n;
   return H2G_OK;
 }
 

@@ -318,6 +318,15 @@ constexpr int kChunkAMma = H2G_MMA_CHUNK_A;        // operator + X doubles per c
 #define H2G_MMA_MIN_COLS 16
 #endif
 constexpr int kMmaMinCols = H2G_MMA_MIN_COLS;      // columns per chunk at least (tall tasks)
+#ifndef H2G_MMA_GROUP
+#define H2G_MMA_GROUP 1
+#endif
+#ifndef H2G_MMA_CHUNK_GROUP
+#define H2G_MMA_CHUNK_GROUP 3072
+#endif
+constexpr bool kMmaGroupMode = H2G_MMA_GROUP != 0;  // wide phases in group mode
+constexpr int kChunkAMmaGroup = H2G_MMA_CHUNK_GROUP; // operator + X doubles per chunk per warp
+                                                      // of the group (group mode)
 static_assert(kMmaConsumers == 4 || kMmaConsumers == 8 || kMmaConsumers == 12, "mma consumers");
 // row groups per size class (rt = 8-row tiles: <= 4, <= 8, <= 16, <= 32)
 constexpr int kMmaWr3 = kMmaConsumers;             // widest class: all warps split rows
@@ -393,7 +402,7 @@ __device__ __forceinline__ void consume_mma(const double* __restrict__ Ab, int l
 template <int KB>
 __global__ void __launch_bounds__(kMmaThreads, kMmaCtasPerSm)
 stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__ cta_begin,
-                  double* arena, int64_t ps) {
+                  double* arena, int64_t ps, int group) {
   constexpr int NT = KB / 8;
   static_assert(KB == 8 || KB == 16, "KB");
   extern __shared__ __align__(128) double smem[];
@@ -414,7 +423,7 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kMmaConsumers);
+      mbar_init(&empty[s], group > 0 ? group : kMmaConsumers);
     }
     for (int r = 0; r < kRecRing; ++r) mbar_init(&recbar[r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -500,6 +509,73 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) c[i][nt][0] = c[i][nt][1] = 0.0;
+  if (group > 0) {
+    // GROUP mode: warps [G st, G st + G) own chunk stream st (chunks i = st
+    // mod S); warp g of the group takes row tiles g, g + G, ... (<= 8, the
+    // host picks G by the phase's largest task) and every k-step, so it
+    // stores its rows at the task's last chunk -- no cross-warp reduction.
+    const int G = group, S = kMmaConsumers / group;
+    const int st = cw / G, g = cw - st * G;
+    for (int i = st; i < n; i += S) {
+      const int s = i % kSlots;
+      mbar_wait(&recbar[i % kRecRing], (uint32_t)(i / kRecRing) & 1u);
+      const ChunkRec& h = rring[i % kRecRing];
+      const int m = h.m;
+      const int ncols = h.ncols;
+      const int flags = h.flags;
+      const int ldas = h.ldas;
+      const int a_shift = h.a_shift;
+      const int odd = h.odd_lda;
+      const int x_base = h.x_base;
+      const int64_t y_off = h.y_off;
+      const int rt = (m + 7) >> 3;
+      const int tpw = g < rt ? (rt - g + G - 1) / G : 0;
+      mbar_wait(&full[s], (uint32_t)(i / kSlots) & 1u);
+      if (ncols > 0 && tpw > 0) {
+        const double* sA = ring + slot_off[s];
+        const int lane_shift = odd ? ((a_shift + kq) & 1) : a_shift;
+        const double* Ab = sA + kq * ldas + lane_shift + rq + 8 * g;
+        const double* Bb = sA + x_base + kq * 8 + rq;
+        const int xps = 8 * ncols;
+        const int ts = 8 * G;
+        switch (tpw) {
+          case 1: consume_mma<1, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
+          case 2: consume_mma<2, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
+          case 3: consume_mma<3, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
+          case 4: consume_mma<4, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
+          default:
+            if constexpr (kMaxTpw > 4) {
+              switch (tpw) {
+                case 5: consume_mma<5, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
+                case 6: consume_mma<6, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
+                case 7: consume_mma<7, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
+                default: consume_mma<8, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
+              }
+            }
+            break;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (flags & kLastOfTask) {
+        double* y = arena + y_off * 8;
+#pragma unroll
+        for (int t = 0; t < kMaxTpw; ++t) {
+          const int row = 8 * (g + G * t) + rq;
+          if (t < tpw && row < m)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              *reinterpret_cast<double2*>(y + nt * ps + (int64_t)row * 8 + 2 * kq) =
+                  make_double2(c[t][nt][0], c[t][nt][1]);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) c[t][nt][0] = c[t][nt][1] = 0.0;
+      }
+    }
+    return;
+  }
   for (int i = 0; i < n; ++i) {
     const int s = i % kSlots;
     mbar_wait(&recbar[i % kRecRing], (uint32_t)(i / kRecRing) & 1u);

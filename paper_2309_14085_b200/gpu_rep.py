@@ -277,6 +277,19 @@ class GpuHierRep:
         return [{"phase": names[i].decode(), "ms": ms[i], "bytes": int(by[i])}
                 for i in range(n.value)]
 
+    def profile_phases_batched(self, kb: int = 16, iters: int = 10):
+        """Per-phase timing of one kb-wide pass of the batched-RHS engine."""
+        cap = 64
+        ms = (C.c_double * cap)()
+        by = (C.c_int64 * cap)()
+        names = (C.c_char_p * cap)()
+        n = C.c_int()
+        _lib.check(self._L.h2g_profile_phases_batched(self._plan, int(kb), int(iters), ms, by,
+                                                      names, cap, C.byref(n)),
+                   "h2g_profile_phases_batched")
+        return [{"phase": names[i].decode(), "ms": ms[i], "bytes": int(by[i])}
+                for i in range(n.value)]
+
 
 def schedule_info(op: PackedOperator, n_sm: int = 148) -> dict:
     """Host-only view of the device schedule (phases, chunks, CTA balance)."""

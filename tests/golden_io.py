@@ -14,8 +14,10 @@ GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def golden_names():
+    # operator fixtures (gmres_*.npz hold solver trajectories, not operators)
     return sorted(os.path.splitext(os.path.basename(p))[0]
-                  for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
+                  for p in glob.glob(os.path.join(GOLDEN_DIR, "g*.npz"))
+                  if not os.path.basename(p).startswith("gmres_"))
 
 
 def load_golden(name):

@@ -127,6 +127,23 @@ def test_batched_rhs_engine(reps, name):
         assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= TOL
 
 
+@pytest.mark.parametrize("name", NAMES)
+def test_batched_group_mode(monkeypatch, name):
+    """Group mode of the batched engine (warps split only rows, no cross-warp
+    reduction; chosen for wide phases) forced on every phase of the golden
+    operators: 16 + 5 RHS equal the single-RHS matvec and the oracle."""
+    from paper_2309_14085_b200.gpu_rep import GpuHierRep
+    op, z, meta = load_golden(name)
+    monkeypatch.setenv("H2G_MMA_GROUP_MIN_TASKS", "1")
+    with GpuHierRep(op) as rep:
+        Q = np.random.default_rng(12).standard_normal((op.N, 21))
+        Phi = rep.matmat(Q)
+        for j in (0, 7, 15, 16, 20):
+            assert rel_err(Phi[:, j], rep.matvec(Q[:, j])) <= 1e-13
+            assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= TOL
+        assert np.array_equal(Phi, rep.matmat(Q))  # bitwise repeatable
+
+
 def test_batched_engine_edge_widths(reps):
     """2 and 9 right-hand sides (zero-padded passes) and a zero block."""
     rep, op, z, meta = reps[NAMES[0]]

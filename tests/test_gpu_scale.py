@@ -43,8 +43,14 @@ def test_parity_at_scale(N, d, kernel, variant, eps):
     with GpuHierRep(op) as rep:
         phi = rep.matvec(q)
         assert np.array_equal(phi, rep.matvec(q))  # bitwise repeatable
+        # batched-RHS engine at scale (group mode on the wide phases): 16 RHS
+        Q = np.random.default_rng(44).standard_normal((N, 16))
+        Q[:, 3] = q
+        Phi = rep.matmat(Q)
+        assert rel_err(Phi[:, 11], rep.matvec(Q[:, 11])) <= 2e-12
     ref = packed_matvec(op, q)
     assert rel_err(phi, ref) <= 1e-12
+    assert rel_err(Phi[:, 3], ref) <= 1e-12
     rows = np.sort(np.random.default_rng(7).choice(N, size=min(N, 128), replace=False))
     exact = dense_matvec_points(pts, op.kernel, q, block=8, rows=rows)
     re_gpu = rel_err(phi[rows], exact)
