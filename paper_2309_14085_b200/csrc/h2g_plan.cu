@@ -855,15 +855,17 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
     // interleaved streams per CTA, with smaller chunks (several in flight per
     // stream).  Narrow phases keep the k-split sharing of every chunk.
     ph.group = 0;
+    int mmax = 0;
     int64_t group_min_tasks = (int64_t)kMmaConsumers * n_cta_ph;
     if (const char* e = getenv("H2G_MMA_GROUP_MIN_TASKS")) group_min_tasks = atoll(e);  // tests
     if (mma && kMmaGroupMode && nt >= group_min_tasks) {
-      int mmax = 0;
       for (int64_t ti = 0; ti < nt; ++ti) mmax = std::max(mmax, (int)s.tasks[ph.task_begin + ti].m);
-      ph.group = std::min(mmax <= 64 ? 1 : (mmax <= 128 ? 2 : 4), kMmaConsumers);
+      ph.group = std::min(std::max(mmax <= 64 ? 1 : (mmax <= 128 ? 2 : 4), kMmaGroupMin),
+                          kMmaConsumers);
     }
-    const int64_t chunk_mma =
-        ph.group > 0 ? std::min(kChunkAMmaGroup * ph.group, kChunkAMma) : kChunkAMma;
+    // (measured, cfg 2 at 16 RHS: 32 KB chunks suit short tasks -- M2L, P2M --
+    // and 24 KB the tall near-field tasks)
+    const int64_t chunk_mma = ph.group > 0 && mmax > 64 ? kChunkAMmaTall : kChunkAMma;
     std::vector<HostChunk> pc;  // this phase's chunks in task order
     std::vector<int64_t> task_chunk0(nt + 1);
     std::vector<double> task_cost(nt);

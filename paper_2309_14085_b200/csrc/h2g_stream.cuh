@@ -307,7 +307,7 @@ __device__ __forceinline__ void consume_stage(const double* __restrict__ As, int
 #define H2G_MMA_RING 11264        // 88 KB data ring per CTA
 #endif
 #ifndef H2G_MMA_CHUNK_A
-#define H2G_MMA_CHUNK_A 3072
+#define H2G_MMA_CHUNK_A 4096
 #endif
 constexpr int kMmaConsumers = H2G_MMA_CONSUMERS;   // consumer warps sharing every chunk
 constexpr int kMmaThreads = 32 * (1 + kMmaConsumers);
@@ -321,12 +321,16 @@ constexpr int kMmaMinCols = H2G_MMA_MIN_COLS;      // columns per chunk at least
 #ifndef H2G_MMA_GROUP
 #define H2G_MMA_GROUP 1
 #endif
-#ifndef H2G_MMA_CHUNK_GROUP
-#define H2G_MMA_CHUNK_GROUP 3072
+#ifndef H2G_MMA_CHUNK_TALL
+#define H2G_MMA_CHUNK_TALL 3072
+#endif
+#ifndef H2G_MMA_GROUP_MIN
+#define H2G_MMA_GROUP_MIN 2
 #endif
 constexpr bool kMmaGroupMode = H2G_MMA_GROUP != 0;  // wide phases in group mode
-constexpr int kChunkAMmaGroup = H2G_MMA_CHUNK_GROUP; // operator + X doubles per chunk per warp
-                                                      // of the group (group mode)
+constexpr int kMmaGroupMin = H2G_MMA_GROUP_MIN;     // smallest group (warps per chunk stream)
+constexpr int kChunkAMmaTall = H2G_MMA_CHUNK_TALL;  // chunk of group-mode phases with tasks
+                                                     // taller than 64 rows
 static_assert(kMmaConsumers == 4 || kMmaConsumers == 8 || kMmaConsumers == 12, "mma consumers");
 // row groups per size class (rt = 8-row tiles: <= 4, <= 8, <= 16, <= 32)
 constexpr int kMmaWr3 = kMmaConsumers;             // widest class: all warps split rows
@@ -431,6 +435,9 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
   __syncthreads();
 
   if (warp == 0) {  // producer: as stream_gemv_kernel, plus the chunk's X by TMA
+    // group mode never reduces across warps: the reduction area (right behind
+    // the ring) extends the ring
+    const int ring_cap = group > 0 ? kRingMma + kMmaConsumers * kRedPerWarp : kRingMma;
     int oldest = 0, head = 0, tail = 0;
     if (lane == 0)
       for (int j = 0; j < kRecAhead && j < n; ++j) {
@@ -458,7 +465,7 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
             break;
           }
           if (head >= tail) {
-            if (kRingMma - head >= need) { off = head; break; }
+            if (ring_cap - head >= need) { off = head; break; }
             if (tail > need) { off = 0; break; }
           } else if (tail - head > need) {
             off = head;
