@@ -165,13 +165,36 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Same, with an L2 cache-policy hint (createpolicy): operator data is read
+// exactly once per pass, so it is streamed evict_first and leaves L2 to the
+// reused vectors (the batched engine's X arena is ~L2-sized).
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // Stage a chunk's operator data: either the record's explicit copy list
 // (lane k issues copy k) or, for a STRIDED RUN (columns of a larger matrix,
 // lda != m), one bulk copy per column: lane k copies column k (16-byte
 // aligned start, so odd offsets carry a one-double shift) to k * ldas.
 // copies[0] then holds {address of A(0, 0), lda, m}.
+template <bool HINT = false>
 __device__ __forceinline__ void issue_operator_copies(const ChunkRec& h, char* st, uint64_t* bar,
-                                                      int lane) {
+                                                      int lane, uint64_t pol = 0) {
   if (h.flags & kStridedRun) {
     if (lane < h.ncols) {
       const CopyDesc cd = h.copies[0];
@@ -179,12 +202,18 @@ __device__ __forceinline__ void issue_operator_copies(const ChunkRec& h, char* s
       const int64_t col = (int64_t)lane * lda;
       const int sh = (int)((h.a_shift + col) & 1);
       const char* src = reinterpret_cast<const char*>(cd.src) + 8 * (col - sh);
-      bulk_g2s(st + 8 * (int64_t)lane * h.ldas, src, (uint32_t)((8 * (sh + (int)cd.bytes) + 15) & ~15),
-               bar);
+      const uint32_t nb = (uint32_t)((8 * (sh + (int)cd.bytes) + 15) & ~15);
+      if constexpr (HINT)
+        bulk_g2s_hint(st + 8 * (int64_t)lane * h.ldas, src, nb, bar, pol);
+      else
+        bulk_g2s(st + 8 * (int64_t)lane * h.ldas, src, nb, bar);
     }
   } else if (lane < h.n_copies) {
     const CopyDesc cd = h.copies[lane];
-    bulk_g2s(st + cd.dst, reinterpret_cast<const void*>(cd.src), cd.bytes, bar);
+    if constexpr (HINT)
+      bulk_g2s_hint(st + cd.dst, reinterpret_cast<const void*>(cd.src), cd.bytes, bar, pol);
+    else
+      bulk_g2s(st + cd.dst, reinterpret_cast<const void*>(cd.src), cd.bytes, bar);
   }
 }
 
@@ -324,6 +353,9 @@ constexpr int kMmaMinCols = H2G_MMA_MIN_COLS;      // columns per chunk at least
 #ifndef H2G_MMA_CHUNK_TALL
 #define H2G_MMA_CHUNK_TALL 3072
 #endif
+#ifndef H2G_MMA_L2HINT
+#define H2G_MMA_L2HINT 1   // operator copies evict_first (X stays in L2)
+#endif
 #ifndef H2G_MMA_GROUP_MIN
 #define H2G_MMA_GROUP_MIN 2
 #endif
@@ -438,6 +470,9 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
     // group mode never reduces across warps: the reduction area (right behind
     // the ring) extends the ring
     const int ring_cap = group > 0 ? kRingMma + kMmaConsumers * kRedPerWarp : kRingMma;
+#if H2G_MMA_L2HINT
+    const uint64_t pol_a = l2_policy_evict_first();
+#endif
     int oldest = 0, head = 0, tail = 0;
     if (lane == 0)
       for (int j = 0; j < kRecAhead && j < n; ++j) {
@@ -485,7 +520,11 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
       }
       off = __shfl_sync(0xffffffffu, off, 0);
       char* st = reinterpret_cast<char*>(ring + off);
+#if H2G_MMA_L2HINT
+      issue_operator_copies<true>(h, st, &full[s], lane, pol_a);
+#else
       issue_operator_copies(h, st, &full[s], lane);
+#endif
       // X plane by plane: [plane][column][8] behind the operator data
       for (int k = lane; k < h.n_seg * NT; k += 32) {
         const int sg = k % h.n_seg, pl = k / h.n_seg;
