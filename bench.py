@@ -234,7 +234,11 @@ def bench_gmres(rep, op, torch, dev, k=16, restart=30, max_iter=300):
     return {"nrhs": k, "restart": restart, "tol": 1e-8, "max_iter": max_iter, "seconds": t,
             "arnoldi_steps": r.iterations, "operator_applications": r.matvecs,
             "ms_per_step": t / max(1, r.iterations) * 1e3, "true_rel_residual_max": true_res,
-            "converged": bool(true_res <= 1e-8)}
+            "converged": bool(true_res <= 1e-8),
+            "note": "unpreconditioned GMRES(30) stagnates on exp(-r^2/0.02) + 1e-6 I; GMRES(30) "
+                    "built from the reference's own solver does too (residual after 300 steps "
+                    "4.6e-10 / 4.7e-4 / 3.2e-2 at N = 1024 / 2048 / 4096, "
+                    "tests/golden/gmres_gauss_ref.npz)"}
 
 
 def bench_variant(op, args, torch, dev, rank, world, recompute=""):
