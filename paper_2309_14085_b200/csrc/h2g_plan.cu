@@ -103,6 +103,14 @@ struct HostSchedule {
   std::vector<Rec4> recs;  // [0, N): points in tree order, then pivot runs
   // terms of the task currently being built (before row splitting)
   std::vector<Term> cur;
+  // per term (until split_heavy_tasks): first row of its block the term's task
+  // covers when the task is a row piece of a taller block, else -1
+  std::vector<int32_t> term_r0;
+  // stored blocks re-laid out as row panels on the device (panelize_tall_blocks)
+  struct Panelized {
+    int64_t base, m, ncols;
+  };
+  std::vector<Panelized> panels;
 };
 
 constexpr int kBlrChunkDoubles = 65536;  // split-K piece of a BLR V^T q product (512 KB)
@@ -111,6 +119,10 @@ constexpr int kBlrChunkDoubles = 65536;  // split-K piece of a BLR V^T q product
 // split-K pieces written to partial slots, combined by a reduce phase that
 // follows (y = [partials] * ones, fixed order).  The split depends only on
 // the schedule, not on the device.
+#ifndef H2G_PANELIZE
+#define H2G_PANELIZE 1
+#endif
+constexpr bool kPanelize = H2G_PANELIZE != 0;  // tall stored blocks as row panels
 constexpr int kMaxSplit = 64;
 constexpr int64_t kSplitCtas = 4 * 296;       // pieces per phase: ~4 per persistent CTA
 constexpr int64_t kSplitMinBytes = 1 << 20;   // never cut below 1 MB pieces
@@ -226,6 +238,7 @@ void emit_task(HostSchedule& s, int64_t y_off, int64_t m, int64_t& bytes, int64_
       Term u = tm;
       if (u.a_space != kRecompute) u.a_off += r0;  // evaluated terms: rows shift via Task.pad
       s.terms.push_back(u);
+      s.term_r0.push_back(m > kMaxRows ? (int32_t)r0 : -1);
       bytes += 8LL * mm * tm.ncols;
     }
     t.t_end = (int32_t)s.terms.size();
@@ -305,6 +318,62 @@ int validate(const h2g_export_desc* d) {
 // Check that an operator [off, off + rows*cols) lies in the blob.
 bool in_blob(const h2g_export_desc* d, int64_t off, int64_t rows, int64_t cols) {
   return off >= 0 && rows >= 0 && cols >= 0 && off + rows * cols <= d->blob_len;
+}
+
+// Blocks taller than kMaxRows are applied as row pieces (emit_task); read in
+// the export's column-major layout every piece is a strided run (one small
+// bulk copy per column).  Re-lay such stored blocks out as ROW PANELS on the
+// device -- panel r0 = rows [r0, r0 + mm) of all columns, column-major with
+// lda = mm, at base + r0 * ncols -- so each piece streams one contiguous run.
+// Only blocks referenced by exactly their row pieces are moved; the device
+// copy is rewritten after upload (unsharded plans).
+void panelize_tall_blocks(HostSchedule& s) {
+  struct Info {
+    int64_t m, ncols, refs;
+    bool ok;
+  };
+  std::map<int64_t, Info> blocks;
+  std::vector<int64_t> base_of(s.terms.size(), -1);
+  for (const Task& t : s.tasks)
+    for (int32_t k = t.t_begin; k < t.t_end; ++k) {
+      const Term& u = s.terms[k];
+      const int32_t r0 = k < (int32_t)s.term_r0.size() ? s.term_r0[k] : -1;
+      if (r0 < 0 || u.a_space != 0 || u.lda <= t.m) continue;
+      const int64_t base = u.a_off - r0;
+      base_of[k] = base;
+      auto it = blocks.find(base);
+      if (it == blocks.end()) {
+        blocks[base] = Info{u.lda, u.ncols, 1, true};
+      } else {
+        Info& b = it->second;
+        b.ok = b.ok && b.m == u.lda && b.ncols == u.ncols;
+        b.refs += 1;
+      }
+    }
+  for (auto& kv : blocks) {
+    Info& b = kv.second;
+    b.ok = b.ok && b.refs == (b.m + kMaxRows - 1) / kMaxRows;
+    if (b.ok) s.panels.push_back({kv.first, b.m, b.ncols});
+  }
+  for (const Task& t : s.tasks)
+    for (int32_t k = t.t_begin; k < t.t_end; ++k) {
+      if (base_of[k] < 0 || !blocks[base_of[k]].ok) continue;
+      Term& u = s.terms[k];
+      const int64_t r0 = s.term_r0[k];
+      u.a_off = base_of[k] + r0 * u.ncols;
+      u.lda = t.m;
+    }
+}
+
+// Host copy of one block in row-panel layout (see panelize_tall_blocks).
+void panel_layout(const double* blk, int64_t m, int64_t ncols, std::vector<double>& out) {
+  out.resize((size_t)(m * ncols));
+  for (int64_t r0 = 0; r0 < m; r0 += kMaxRows) {
+    const int64_t mm = std::min<int64_t>(kMaxRows, m - r0);
+    double* dst = out.data() + r0 * ncols;
+    for (int64_t c = 0; c < ncols; ++c)
+      for (int64_t r = 0; r < mm; ++r) dst[c * mm + r] = blk[c * m + r0 + r];
+  }
 }
 
 // Cut heavy tasks into split-K pieces (partial slots appended to the arena)
@@ -828,6 +897,8 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
   }
   s.phases.back().alg_bytes = bytes;
   end_phase(s);
+  if (sh.nranks == 1 && kPanelize) panelize_tall_blocks(s);
+  s.term_r0.clear();
   split_heavy_tasks(s, p->n_slots, ones_off);
   partition_engines(s);
   return H2G_OK;
@@ -1397,6 +1468,12 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     } else {
       p->blob_len = d->blob_len;
       if ((r = upload((void**)&p->d_blob, d->blob, sizeof(double) * d->blob_len))) return r;
+      std::vector<double> pan;
+      for (const auto& b : s.panels) {  // tall blocks -> row panels (panelize_tall_blocks)
+        panel_layout(d->blob + b.base, b.m, b.ncols, pan);
+        CUDA_TRY(cudaMemcpy(p->d_blob + b.base, pan.data(), sizeof(double) * pan.size(),
+                            cudaMemcpyHostToDevice));
+      }
     }
     if (nranks > 1) {  // exchange copy lists
       int64_t mx = 0;
@@ -1907,6 +1984,14 @@ int h2g_schedule_build(const h2g_export_desc* desc, int rank, int nranks, h2g_sc
   if (rc) return rc;
   h2g_sched* o = new h2g_sched();
   if (nranks > 1) compact_blob(desc, s, o->blob);
+  if (!s.panels.empty()) {  // the blob the device holds: tall blocks as row panels
+    o->blob.assign(desc->blob, desc->blob + desc->blob_len);
+    std::vector<double> pan;
+    for (const auto& b : s.panels) {
+      panel_layout(desc->blob + b.base, b.m, b.ncols, pan);
+      std::copy(pan.begin(), pan.end(), o->blob.begin() + b.base);
+    }
+  }
   auto& T = o->i64["tasks"];
   for (const Task& t : s.tasks) {
     T.push_back(t.y_off);

@@ -62,3 +62,20 @@ def test_parity_at_scale(N, d, kernel, variant, eps):
         # it for H2*(b+t) (1.1e-5 at eps 1e-8, identical for oracle and GPU; the
         # native build equals the reference build, tests/test_builder.py).
         assert re_gpu <= 100 * eps
+
+
+@pytest.mark.parametrize("variant", ["h2star-bt", "h2plusH-star"])
+def test_tall_blocks_as_row_panels(variant):
+    """Near blocks taller than 256 rows (leaves of up to 400 points) stream as
+    row panels (contiguous pieces): single- and 16-RHS results equal the
+    oracle on the export's own layout."""
+    from paper_2309_14085_b200.gpu_rep import GpuHierRep
+    op = build_variant(variant, uniform_points(6000, 2, 42), "log2d", 400, 1e-8)
+    q = np.random.default_rng(43).standard_normal(op.N)
+    ref = packed_matvec(op, q)
+    Q = np.random.default_rng(3).standard_normal((op.N, 16))
+    with GpuHierRep(op) as rep:
+        assert rel_err(rep.matvec(q), ref) <= 1e-12
+        Phi = rep.matmat(Q)
+    for j in (0, 9, 15):
+        assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= 1e-12

@@ -94,3 +94,21 @@ def test_split_k_heavy_tasks(monkeypatch, name, nranks):
     n_red = int((v["phases"][:, 3] == 0).sum()) - int((plain[:, 3] == 0).sum())
     assert n_red >= 1 and len(v["phases"]) == len(plain) + n_red
     assert rel_err(emulate_matvec(op, z["q"], nranks), z["phi_ref"]) <= 1e-13
+
+
+@pytest.mark.parametrize("variant", ["h2star-bt", "h2plusH-star"])
+def test_tall_blocks_as_row_panels(variant):
+    """Leaves of up to 400 points make near blocks taller than the 256-row task
+    limit: the unsharded schedule applies them as row pieces of blocks moved
+    to row-panel layout (panelize_tall_blocks); the schedule over that blob
+    equals the oracle, and a sharded schedule (no panels) too."""
+    from oracle.packed_matvec import packed_matvec
+    from paper_2309_14085_b200.builder import build_variant, uniform_points
+    op = build_variant(variant, uniform_points(6000, 2, 42), "log2d", 400, 1e-8)
+    q = np.random.default_rng(43).standard_normal(op.N)
+    ref = packed_matvec(op, q)
+    view = schedule_view(op, 0, 1)
+    assert len(view["blob"]) == len(op.blob)            # row panels applied
+    assert not np.array_equal(view["blob"], op.blob)
+    assert rel_err(emulate_matvec(op, q, 1), ref) <= 1e-13
+    assert rel_err(emulate_matvec(op, q, 2), ref) <= 1e-13
