@@ -931,8 +931,11 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
     if (const char* e = getenv("H2G_MMA_GROUP_MIN_TASKS")) group_min_tasks = atoll(e);  // tests
     if (mma && kMmaGroupMode && nt >= group_min_tasks) {
       for (int64_t ti = 0; ti < nt; ++ti) mmax = std::max(mmax, (int)s.tasks[ph.task_begin + ti].m);
-      ph.group = std::min(std::max(mmax <= 64 ? 1 : (mmax <= 128 ? 2 : 4), kMmaGroupMin),
-                          kMmaConsumers);
+      // smallest power of two >= kMmaGroupMin giving every warp <= kMaxTpw tiles
+      const int rt = (mmax + 7) / 8;
+      int g = std::max(1, kMmaGroupMin);
+      while (g < kMmaConsumers && (rt + g - 1) / g > kMaxTpw) g *= 2;
+      ph.group = (rt + g - 1) / g <= kMaxTpw && g <= kMmaConsumers ? g : 0;
     }
     // (measured, cfg 2 at 16 RHS: 32 KB chunks suit short tasks -- M2L, P2M --
     // and 24 KB the tall near-field tasks)
