@@ -193,3 +193,24 @@ def test_pinned_host_calls_use_cached_graph(reps):
     out2 = torch.empty(op.N, dtype=torch.float64).pin_memory().numpy()
     assert rel_err(rep.matvec(q2, out=out2), 2 * ref) <= 1e-15
     assert np.array_equal(rep.matvec(q, out=out), ref)
+
+
+def test_phase_profilers(reps):
+    """h2g_profile_phases / h2g_profile_phases_batched (the per-phase timings
+    bench.py and tools/mma_phases.py report): every phase timed, bytes match
+    the single-RHS plan's phases, and the arena still gives correct results
+    afterwards."""
+    import torch
+    rep, op, z, meta = reps["g2d_log_h2star"]
+    q = torch.from_numpy(z["q"]).cuda()
+    phi = torch.empty_like(q)
+    single = rep.profile_phases(q, phi, iters=2)
+    assert single[0]["phase"] == "gather" and single[-1]["phase"] == "scatter"
+    assert all(r["ms"] > 0 for r in single)
+    for kb in (8, 16):
+        rows = rep.profile_phases_batched(kb, iters=2)
+        assert rows and all(r["ms"] > 0 for r in rows)
+        inner = {r["phase"]: r["bytes"] for r in single[1:-1]}
+        for r in rows:
+            assert r["bytes"] == inner.get(r["phase"], r["bytes"])
+    assert rel_err(rep.matvec(z["q"]), z["phi_ref"]) <= TOL
