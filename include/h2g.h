@@ -192,6 +192,8 @@ typedef struct h2g_shard_info {
   int64_t send_slots;          /* doubles this rank contributes to the exchange */
   int64_t max_send_slots;      /* per-rank stride of the all-gather buffer */
   int64_t blob_bytes;          /* operator bytes resident on this rank */
+  int64_t halo_slots;          /* x-halo doubles this rank contributes (distributed q) */
+  int64_t max_halo_slots;      /* per-rank stride of the x-halo all-gather buffer */
 } h2g_shard_info;
 
 int h2g_plan_create_sharded(const h2g_export_desc* desc, int device, int rank, int nranks,
@@ -202,13 +204,32 @@ int h2g_shard_pack(h2g_plan* plan, double* send_dev, void* stream);
 int h2g_shard_unpack(h2g_plan* plan, const double* recv_dev, void* stream);
 int h2g_matvec_end(h2g_plan* plan, double* phi_dev, int64_t n, void* stream);
 
+/* Distributed vectors: q and phi live as each rank's OWN tree-order rows
+ * [row_begin, row_end) (points perm[row_begin .. row_end)), no replicated q.
+ * One matvec:  h2g_shard_load_q(q_own)  ->  h2g_halo_pack(hsend)  ->
+ * all-gather (max_halo_slots doubles per rank, rank-major) into hrecv  ->
+ * h2g_halo_unpack(hrecv)  ->  h2g_shard_part0  ->  h2g_shard_pack / all-gather
+ * / h2g_shard_unpack (as above)  ->  h2g_shard_store_phi(phi_own).  The x
+ * halo is the q rows other ranks read: near-field sources and the BLR V^T
+ * sources of owned targets across subtree boundaries. */
+int h2g_shard_load_q(h2g_plan* plan, const double* q_own_dev, void* stream);
+int h2g_halo_pack(h2g_plan* plan, double* send_dev, void* stream);
+int h2g_halo_unpack(h2g_plan* plan, const double* recv_dev, void* stream);
+int h2g_shard_part0(h2g_plan* plan, void* stream);
+int h2g_shard_store_phi(h2g_plan* plan, double* phi_own_dev, void* stream);
+
 /* Host-only view of rank `rank`'s schedule (no CUDA; emulation and tests):
- * named int64 arrays "tasks" [n x 4: y_off, m, t_begin, t_end], "terms"
- * [n x 5: a_off, x_off, lda, ncols, a_space], "phases" [n x 4: task_begin,
- * task_end, part, alg_bytes], "pack" / "unpack" [n x 3: src, dst, len],
- * "meta" [n_slots, q_tree, phi_tree, ones_off, n_ones, row_begin, row_end,
- * send_slots, max_send_slots, level] and the compacted f64 "blob" (empty when
- * nranks == 1: terms index the export's blob). */
+ * named int64 arrays "tasks" [n x 5: y_off, m, t_begin, t_end, row_rec],
+ * "terms" [n x 6: a_off, x_off, lda, ncols, a_space, self], "phases" [n x 4:
+ * task_begin, task_end, part, alg_bytes], "pack" / "unpack" [n x 3: src, dst,
+ * len], "halo" [n x 3: sending rank, tree row, len] (the x-halo ranges of
+ * every rank), "meta" [n_slots, q_tree, phi_tree, ones_off, n_ones, row_begin,
+ * row_end, send_slots, max_send_slots, level], the compacted f64 "blob"
+ * (empty when nranks == 1 and no block was re-laid out: terms index the
+ * export's blob) and the f64 point records "recs" [n x 4] of kernel-evaluated
+ * terms.  a_space: 0 blob, 1 arena, 2 evaluated = K[records row_rec .. + m,
+ * records a_off .. + ncols] (self = 1: rows and columns are the same records,
+ * the i == j rule applies). */
 typedef struct h2g_sched h2g_sched;
 int h2g_schedule_build(const h2g_export_desc* desc, int rank, int nranks, h2g_sched** out);
 int h2g_schedule_get(const h2g_sched* sched, const char* name, const void** ptr, int64_t* len,

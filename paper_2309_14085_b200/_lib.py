@@ -55,7 +55,8 @@ class ShardInfo(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("level", C.c_int32),
                 ("pad", C.c_int32), ("row_begin", C.c_int64), ("row_end", C.c_int64),
                 ("send_slots", C.c_int64), ("max_send_slots", C.c_int64),
-                ("blob_bytes", C.c_int64)]
+                ("blob_bytes", C.c_int64), ("halo_slots", C.c_int64),
+                ("max_halo_slots", C.c_int64)]
 
 
 # every symbol include/h2g.h declares (checked by tests/test_abi.py)
@@ -65,7 +66,9 @@ H2G_SYMBOLS = ("h2g_plan_create", "h2g_plan_destroy", "h2g_plan_get_stats", "h2g
                "h2g_error_string", "h2g_last_error_detail", "h2g_abi_version",
                "h2g_plan_create_sharded", "h2g_shard_get_info", "h2g_matvec_begin",
                "h2g_shard_pack", "h2g_shard_unpack", "h2g_matvec_end",
-               "h2g_schedule_build", "h2g_schedule_get", "h2g_schedule_free")
+               "h2g_schedule_build", "h2g_schedule_get", "h2g_schedule_free",
+               "h2g_shard_load_q", "h2g_halo_pack", "h2g_halo_unpack", "h2g_shard_part0",
+               "h2g_shard_store_phi")
 
 _LIB = None
 
@@ -107,6 +110,9 @@ def load(path: str = None) -> C.CDLL:
     L.h2g_shard_pack.argtypes = [vp, vp, vp]
     L.h2g_shard_unpack.argtypes = [vp, vp, vp]
     L.h2g_matvec_end.argtypes = [vp, vp, C.c_int64, vp]
+    for name in ("h2g_shard_load_q", "h2g_halo_pack", "h2g_halo_unpack", "h2g_shard_store_phi"):
+        getattr(L, name).argtypes = [vp, vp, vp]
+    L.h2g_shard_part0.argtypes = [vp, vp]
     L.h2g_schedule_build.argtypes = [C.POINTER(ExportDesc), C.c_int, C.c_int, C.POINTER(vp)]
     L.h2g_schedule_get.argtypes = [vp, C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int32)]

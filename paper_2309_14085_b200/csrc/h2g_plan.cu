@@ -159,6 +159,14 @@ struct h2g_plan {
   Shard shard;
   std::vector<std::vector<std::pair<int64_t, int64_t>>> xchg;  // per rank: (slot, len) ranges
   int64_t send_slots = 0, max_send_slots = 0;
+  // x halo (distributed q): per rank the tree-order row ranges of q it owns
+  // and some other rank reads (near sources, BLR V^T sources across subtree
+  // boundaries); all-gathered before part 0 (h2g_halo_pack / _unpack)
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> xhalo;
+  int64_t halo_slots = 0, max_halo_slots = 0;
+  CopyRange* d_hpack = nullptr;
+  CopyRange* d_hunpack = nullptr;
+  int n_hpack = 0, n_hunpack = 0;
   CopyRange* d_pack = nullptr;      // this rank's ranges -> send buffer
   CopyRange* d_unpack = nullptr;    // other ranks' ranges: recv buffer -> arena
   int n_pack = 0, n_unpack = 0;
@@ -219,6 +227,12 @@ struct h2g_plan {
   double* d_hq = nullptr;    // host-call staging (h2g_matvec_host)
   double* d_hphi = nullptr;
   size_t h_cap = 0;
+  // Cross-stream ordering: every call shares the arena / counters, so a call
+  // on a different stream than the previous one first waits for the previous
+  // call's completion event (device-side, no host sync).
+  cudaEvent_t ev_done = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool ev_pending = false;
 };
 
 namespace {
@@ -663,6 +677,68 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
         const int64_t pr = d->blr_rank[k];
         for (size_t i = 0; i < pieces[k].size(); ++i)
           if (pieces[k][i].owner == r) rr.push_back({part_off[k] + (int64_t)i * pr, pr});
+      }
+    }
+  }
+
+  // ---- x halo: q rows each rank reads outside its own rows ----
+  // rank q reads q_tree rows of: its own leaves (P2M, near self), the near
+  // sources of its leaves, the sources Y of BLR factors whose target X it
+  // owns (level >= L_s; replicated-target factors are cut at the rank row
+  // bounds, so those pieces read own rows only).  Owner r of a row range
+  // sends it when another rank needs it.
+  p->xhalo.assign(sh.nranks, {});
+  if (sh.nranks > 1) {
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> need(sh.nranks);
+    for (int64_t x = lo[kappa]; x < lo[kappa + 1]; ++x) {
+      const int q = sh.owner(x - lo[kappa], kappa);
+      for (int64_t k = d->near_rowptr[x]; k < d->near_rowptr[x + 1]; ++k) {
+        const int64_t y = d->near_src[k];
+        if (y >= 0 && y < nc && nsz(y) > 0) need[q].push_back({st[y], en[y]});
+      }
+    }
+    for (int64_t k = 0; k < blr_nnz; ++k) {
+      const int lx = level_of(blr_x[k]);
+      if (lx < Ls) continue;
+      const int q = sh.owner(blr_x[k] - lo[lx], lx);
+      const int64_t y = d->blr_src[k];
+      if (nsz(y) > 0) need[q].push_back({st[y], en[y]});
+    }
+    for (int q = 0; q < sh.nranks; ++q) {  // outside own rows, merged
+      std::vector<std::pair<int64_t, int64_t>> iv;
+      for (auto& v : need[q]) {
+        const int64_t a = v.first, b = v.second;
+        const int64_t o0 = sh.row_bound[q], o1 = sh.row_bound[q + 1];
+        if (a < o0) iv.push_back({a, std::min(b, o0)});
+        if (b > o1) iv.push_back({std::max(a, o1), b});
+      }
+      std::sort(iv.begin(), iv.end());
+      std::vector<std::pair<int64_t, int64_t>> m;
+      for (auto& v : iv) {
+        if (v.second <= v.first) continue;
+        if (!m.empty() && v.first <= m.back().second)
+          m.back().second = std::max(m.back().second, v.second);
+        else
+          m.push_back(v);
+      }
+      need[q].swap(m);
+    }
+    for (int r = 0; r < sh.nranks; ++r) {  // what r sends: others' needs inside r's rows
+      std::vector<std::pair<int64_t, int64_t>> iv;
+      const int64_t o0 = sh.row_bound[r], o1 = sh.row_bound[r + 1];
+      for (int q = 0; q < sh.nranks; ++q)
+        if (q != r)
+          for (auto& v : need[q]) {
+            const int64_t a = std::max(v.first, o0), b = std::min(v.second, o1);
+            if (b > a) iv.push_back({a, b});
+          }
+      std::sort(iv.begin(), iv.end());
+      for (auto& v : iv) {
+        auto& m = p->xhalo[r];
+        if (!m.empty() && v.first <= m.back().first + m.back().second)
+          m.back().second = std::max(m.back().first + m.back().second, v.second) - m.back().first;
+        else
+          m.push_back({v.first, v.second - v.first});  // (row, len)
       }
     }
   }
@@ -1260,9 +1336,24 @@ int check_vec_args(h2g_plan* p, int64_t n, int64_t nrhs, int64_t ld) {
   return H2G_OK;
 }
 
+// Order this call's stream after the previous call's work when they differ.
+int join_stream(h2g_plan* p, cudaStream_t s) {
+  if (p->ev_pending && s != p->last_stream) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_done, 0));
+  return H2G_OK;
+}
+
+// The call's work on `s` is the plan's latest: later calls on other streams wait for it.
+int mark_stream(h2g_plan* p, cudaStream_t s) {
+  CUDA_TRY(cudaEventRecord(p->ev_done, s));
+  p->last_stream = s;
+  p->ev_pending = true;
+  return H2G_OK;
+}
+
 void free_plan(h2g_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
+  if (p->ev_done) cudaEventDestroy(p->ev_done);
   if (p->hg_exec) cudaGraphExecDestroy(p->hg_exec);
   if (p->hg_graph) cudaGraphDestroy(p->hg_graph);
   if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
@@ -1270,6 +1361,8 @@ void free_plan(h2g_plan* p) {
   if (p->graph1) cudaGraphDestroy(p->graph1);
   cudaFree(p->d_pack);
   cudaFree(p->d_unpack);
+  cudaFree(p->d_hpack);
+  cudaFree(p->d_hunpack);
   if (p->graph) cudaGraphDestroy(p->graph);
   cudaFree(p->d_blob);
   cudaFree(p->d_arena);
@@ -1298,7 +1391,7 @@ void free_plan(h2g_plan* p) {
 }
 
 // Shard ownership for (rank, nranks): L_s = the first level with >= 4
-// subtrees per rank (capped at kappa); rank r owns the Morton range
+// subtrees per rank and at least 3 (capped at kappa); rank r owns the Morton range
 // [r*S/R, (r+1)*S/R) of the S = 2^(d*L_s) subtrees.
 // Do two distinct points share coordinates?  (Then r == 0 can occur off the
 // diagonal and every evaluated entry needs the zero_value test.)
@@ -1329,8 +1422,15 @@ Shard make_shard(const h2g_export_desc* d, int rank, int nranks) {
   sh.nranks = nranks;
   sh.dim = d->dim;
   sh.level = 1;
-  if (nranks > 1)
+  if (nranks > 1) {
+    // at least 4 subtrees per rank, and level 3 when the tree is that deep
+    // (north_star / SURVEY §8(e): 3D subtrees at level 3, 512 of them, a
+    // contiguous 1/8 of them per GPU at 8 GPUs); H2G_SHARD_LEVEL overrides
     while (sh.level < d->kappa && (1LL << (d->dim * sh.level)) < 4LL * nranks) ++sh.level;
+    sh.level = std::max(sh.level, std::min(3, d->kappa));
+    if (const char* e = getenv("H2G_SHARD_LEVEL"))
+      sh.level = std::max(1, std::min(d->kappa, atoi(e)));
+  }
   const int64_t S = 1LL << (d->dim * sh.level);
   sh.sub_lo.resize(nranks + 1);
   sh.row_bound.resize(nranks + 1);
@@ -1462,6 +1562,7 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
   };
   rc = [&]() -> int {
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
     int r;
     if (nranks > 1) {
       p->blob_len = (int64_t)local_blob.size();
@@ -1501,6 +1602,31 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
       }
       p->n_pack = (int)pack.size();
       p->n_unpack = (int)unpack.size();
+      {  // x halo copy lists: own rows -> send, others' rows -> arena q_tree
+        int64_t hm = 0;
+        for (int q = 0; q < nranks; ++q) {
+          int64_t tot = 0;
+          for (auto& rg : p->xhalo[q]) tot += rg.second;
+          hm = std::max(hm, tot);
+        }
+        p->max_halo_slots = hm;
+        std::vector<CopyRange> hp, hu;
+        for (int q = 0; q < nranks; ++q) {
+          int64_t pos = 0;
+          for (auto& rg : p->xhalo[q]) {
+            if (q == rank)
+              hp.push_back({p->q_tree + rg.first, pos, rg.second});
+            else
+              hu.push_back({(int64_t)q * hm + pos, p->q_tree + rg.first, rg.second});
+            pos += rg.second;
+          }
+          if (q == rank) p->halo_slots = pos;
+        }
+        p->n_hpack = (int)hp.size();
+        p->n_hunpack = (int)hu.size();
+        if ((r = upload((void**)&p->d_hpack, hp.data(), sizeof(CopyRange) * hp.size()))) return r;
+        if ((r = upload((void**)&p->d_hunpack, hu.data(), sizeof(CopyRange) * hu.size()))) return r;
+      }
       if ((r = upload((void**)&p->d_pack, pack.data(), sizeof(CopyRange) * pack.size()))) return r;
       if ((r = upload((void**)&p->d_unpack, unpack.data(), sizeof(CopyRange) * unpack.size())))
         return r;
@@ -1698,6 +1824,9 @@ inline int batch_which(const h2g_plan* p, int64_t nrhs) {
   return nrhs > 8 ? 1 : 0;
 }
 
+int matvec_body(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nrhs, int64_t ld,
+                cudaStream_t s);
+
 int matvec_impl(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nrhs, int64_t ld,
                 cudaStream_t s) {
   int rc = check_vec_args(p, n, nrhs, ld);
@@ -1706,6 +1835,15 @@ int matvec_impl(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nr
   CUDA_TRY(cudaSetDevice(p->device));
   if (p->shard.nranks > 1)
     return fail(H2G_ERR_INVALID_ARG, "sharded plan: use h2g_matvec_begin / exchange / end");
+  if ((rc = join_stream(p, s))) return rc;
+  rc = matvec_body(p, q, phi, n, nrhs, ld, s);
+  if (rc) return rc;
+  return mark_stream(p, s);
+}
+
+int matvec_body(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nrhs, int64_t ld,
+                cudaStream_t s) {
+  int rc = H2G_OK;
   if (nrhs > 1 && p->engine == 1 && p->use_batched) {
     for (int64_t c0 = 0; c0 < nrhs;) {
       const int which = batch_which(p, nrhs - c0);
@@ -1790,6 +1928,8 @@ int h2g_shard_get_info(const h2g_plan* p, h2g_shard_info* o) {
   o->send_slots = p->send_slots;
   o->max_send_slots = p->max_send_slots;
   o->blob_bytes = 8 * p->blob_len;
+  o->halo_slots = p->halo_slots;
+  o->max_halo_slots = p->max_halo_slots;
   return H2G_OK;
 }
 
@@ -1799,11 +1939,16 @@ int h2g_matvec_begin(h2g_plan* p, const double* q_dev, int64_t n, void* stream) 
   if (!q_dev) return fail(H2G_ERR_INVALID_ARG, "null vector");
   CUDA_TRY(cudaSetDevice(p->device));
   cudaStream_t s = (cudaStream_t)stream;
+  int rc = join_stream(p, s);
+  if (rc) return rc;
   gather_perm_kernel<<<grid_for(n), 256, 0, s>>>(q_dev, 1, p->d_perm, p->d_arena + p->q_tree, n);
   CUDA_TRY(cudaGetLastError());
-  if (p->shard.nranks == 1) return run_middle(p, s);  // unsharded: everything here
+  if (p->shard.nranks == 1) {  // unsharded: everything here
+    if ((rc = run_middle(p, s))) return rc;
+    return mark_stream(p, s);
+  }
   CUDA_TRY(cudaGraphLaunch(p->graph_exec, s));
-  return H2G_OK;
+  return mark_stream(p, s);
 }
 
 int h2g_shard_pack(h2g_plan* p, double* send_dev, void* stream) {
@@ -1811,10 +1956,12 @@ int h2g_shard_pack(h2g_plan* p, double* send_dev, void* stream) {
   if (p->n_pack == 0) return H2G_OK;
   if (!send_dev) return fail(H2G_ERR_INVALID_ARG, "null buffer");
   CUDA_TRY(cudaSetDevice(p->device));
+  int rc = join_stream(p, (cudaStream_t)stream);
+  if (rc) return rc;
   copy_ranges_kernel<<<std::min(p->n_pack, 1024), 256, 0, (cudaStream_t)stream>>>(
       p->d_pack, p->n_pack, p->d_arena, send_dev);
   CUDA_TRY(cudaGetLastError());
-  return H2G_OK;
+  return mark_stream(p, (cudaStream_t)stream);
 }
 
 int h2g_shard_unpack(h2g_plan* p, const double* recv_dev, void* stream) {
@@ -1822,10 +1969,12 @@ int h2g_shard_unpack(h2g_plan* p, const double* recv_dev, void* stream) {
   if (p->n_unpack == 0) return H2G_OK;
   if (!recv_dev) return fail(H2G_ERR_INVALID_ARG, "null buffer");
   CUDA_TRY(cudaSetDevice(p->device));
+  int rc = join_stream(p, (cudaStream_t)stream);
+  if (rc) return rc;
   copy_ranges_kernel<<<std::min(p->n_unpack, 1024), 256, 0, (cudaStream_t)stream>>>(
       p->d_unpack, p->n_unpack, recv_dev, p->d_arena);
   CUDA_TRY(cudaGetLastError());
-  return H2G_OK;
+  return mark_stream(p, (cudaStream_t)stream);
 }
 
 int h2g_matvec_end(h2g_plan* p, double* phi_dev, int64_t n, void* stream) {
@@ -1834,6 +1983,8 @@ int h2g_matvec_end(h2g_plan* p, double* phi_dev, int64_t n, void* stream) {
   if (!phi_dev) return fail(H2G_ERR_INVALID_ARG, "null vector");
   CUDA_TRY(cudaSetDevice(p->device));
   cudaStream_t s = (cudaStream_t)stream;
+  int rc = join_stream(p, s);
+  if (rc) return rc;
   if (p->shard.nranks > 1) CUDA_TRY(cudaGraphLaunch(p->graph1_exec, s));
   const int64_t rows = p->row_end - p->row_begin;
   if (rows > 0) {
@@ -1841,7 +1992,73 @@ int h2g_matvec_end(h2g_plan* p, double* phi_dev, int64_t n, void* stream) {
                                                        phi_dev, 1, p->row_begin, p->row_end);
     CUDA_TRY(cudaGetLastError());
   }
-  return H2G_OK;
+  return mark_stream(p, s);
+}
+
+int h2g_shard_load_q(h2g_plan* p, const double* q_own_dev, void* stream) {
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  const int64_t rows = p->row_end - p->row_begin;
+  if (rows > 0 && !q_own_dev) return fail(H2G_ERR_INVALID_ARG, "null vector");
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = join_stream(p, s);
+  if (rc) return rc;
+  if (rows > 0)
+    CUDA_TRY(cudaMemcpyAsync(p->d_arena + p->q_tree + p->row_begin, q_own_dev,
+                             sizeof(double) * rows, cudaMemcpyDeviceToDevice, s));
+  return mark_stream(p, s);
+}
+
+int h2g_halo_pack(h2g_plan* p, double* send_dev, void* stream) {
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  if (p->n_hpack == 0) return H2G_OK;
+  if (!send_dev) return fail(H2G_ERR_INVALID_ARG, "null buffer");
+  CUDA_TRY(cudaSetDevice(p->device));
+  int rc = join_stream(p, (cudaStream_t)stream);
+  if (rc) return rc;
+  copy_ranges_kernel<<<std::min(p->n_hpack, 1024), 256, 0, (cudaStream_t)stream>>>(
+      p->d_hpack, p->n_hpack, p->d_arena, send_dev);
+  CUDA_TRY(cudaGetLastError());
+  return mark_stream(p, (cudaStream_t)stream);
+}
+
+int h2g_halo_unpack(h2g_plan* p, const double* recv_dev, void* stream) {
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  if (p->n_hunpack == 0) return H2G_OK;
+  if (!recv_dev) return fail(H2G_ERR_INVALID_ARG, "null buffer");
+  CUDA_TRY(cudaSetDevice(p->device));
+  int rc = join_stream(p, (cudaStream_t)stream);
+  if (rc) return rc;
+  copy_ranges_kernel<<<std::min(p->n_hunpack, 1024), 256, 0, (cudaStream_t)stream>>>(
+      p->d_hunpack, p->n_hunpack, recv_dev, p->d_arena);
+  CUDA_TRY(cudaGetLastError());
+  return mark_stream(p, (cudaStream_t)stream);
+}
+
+int h2g_shard_part0(h2g_plan* p, void* stream) {
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  if (p->shard.nranks == 1) return fail(H2G_ERR_INVALID_ARG, "not a sharded plan");
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = join_stream(p, s);
+  if (rc) return rc;
+  CUDA_TRY(cudaGraphLaunch(p->graph_exec, s));
+  return mark_stream(p, s);
+}
+
+int h2g_shard_store_phi(h2g_plan* p, double* phi_own_dev, void* stream) {
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  const int64_t rows = p->row_end - p->row_begin;
+  if (rows > 0 && !phi_own_dev) return fail(H2G_ERR_INVALID_ARG, "null vector");
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = join_stream(p, s);
+  if (rc) return rc;
+  if (p->shard.nranks > 1) CUDA_TRY(cudaGraphLaunch(p->graph1_exec, s));
+  if (rows > 0)
+    CUDA_TRY(cudaMemcpyAsync(phi_own_dev, p->d_arena + p->phi_tree + p->row_begin,
+                             sizeof(double) * rows, cudaMemcpyDeviceToDevice, s));
+  return mark_stream(p, s);
 }
 
 int h2g_plan_destroy(h2g_plan* plan) {
@@ -1895,6 +2112,7 @@ int h2g_matvec_host(h2g_plan* p, const double* q_host, double* phi_host, int64_t
   if (rc) return rc;
   if (!q_host || !phi_host) return fail(H2G_ERR_INVALID_ARG, "null vector");
   CUDA_TRY(cudaSetDevice(p->device));
+  if ((rc = join_stream(p, p->stream))) return rc;  // after work queued on a caller stream
   const size_t elems = (size_t)n * (size_t)ld;
   const size_t bytes = sizeof(double) * elems;
   if (p->h_cap < elems) {  // persistent device staging for host-pointer calls
@@ -1952,6 +2170,7 @@ int h2g_matvec_host(h2g_plan* p, const double* q_host, double* phi_host, int64_t
       p->hg_phi = phi_host;
     }
     CUDA_TRY(cudaGraphLaunch(p->hg_exec, p->stream));
+    if ((rc = mark_stream(p, p->stream))) return rc;
     CUDA_TRY(cudaStreamSynchronize(p->stream));
     return H2G_OK;
   }
@@ -1971,6 +2190,7 @@ int h2g_matvec_host(h2g_plan* p, const double* q_host, double* phi_host, int64_t
 struct h2g_sched {
   std::map<std::string, std::vector<int64_t>> i64;
   std::vector<double> blob;
+  std::vector<double> recs;  // P2P point records (x, y, z, w) of evaluated terms
 };
 
 extern "C" {
@@ -2001,6 +2221,7 @@ int h2g_schedule_build(const h2g_export_desc* desc, int rank, int nranks, h2g_sc
     T.push_back(t.m);
     T.push_back(t.t_begin);
     T.push_back(t.t_end);
+    T.push_back(is_p2p_task(s, t) ? (int64_t)t.pad : -1);  // row record of an evaluated task
   }
   auto& M = o->i64["terms"];
   for (const Term& t : s.terms) {
@@ -2009,6 +2230,14 @@ int h2g_schedule_build(const h2g_export_desc* desc, int rank, int nranks, h2g_sc
     M.push_back(t.lda);
     M.push_back(t.ncols);
     M.push_back(t.a_space);
+    M.push_back(t.a_space == kRecompute ? (int64_t)t.pad : 0);  // self block (i == j rule)
+  }
+  o->recs.resize(4 * s.recs.size());
+  for (size_t i = 0; i < s.recs.size(); ++i) {
+    o->recs[4 * i] = s.recs[i].x;
+    o->recs[4 * i + 1] = s.recs[i].y;
+    o->recs[4 * i + 2] = s.recs[i].z;
+    o->recs[4 * i + 3] = s.recs[i].w;
   }
   auto& P = o->i64["phases"];
   for (const Phase& ph : s.phases) {
@@ -2038,6 +2267,11 @@ int h2g_schedule_build(const h2g_export_desc* desc, int rank, int nranks, h2g_sc
     }
     if (q == rank) send = pos;
   }
+  {  // x halo: every rank's (row, len) send ranges, rank-major: [rank, row, len]
+    auto& H = o->i64["halo"];
+    for (int q = 0; q < (int)tmp.xhalo.size(); ++q)
+      for (auto& rg : tmp.xhalo[q]) H.insert(H.end(), {(int64_t)q, rg.first, rg.second});
+  }
   o->i64["meta"] = {tmp.n_slots, tmp.q_tree, tmp.phi_tree, tmp.ones_off, tmp.n_ones,
                     tmp.shard.row_bound[rank], tmp.shard.row_bound[rank + 1], send, mx,
                     tmp.shard.level};
@@ -2049,9 +2283,10 @@ int h2g_schedule_get(const h2g_sched* sc, const char* name, const void** ptr, in
                      int32_t* is_f64) {
   if (!sc || !name || !ptr || !len || !is_f64) return fail(H2G_ERR_INVALID_ARG, "bad argument");
   const std::string n(name);
-  if (n == "blob") {
-    *ptr = sc->blob.data();
-    *len = (int64_t)sc->blob.size();
+  if (n == "blob" || n == "recs") {
+    const std::vector<double>& v = n == "blob" ? sc->blob : sc->recs;
+    *ptr = v.data();
+    *len = (int64_t)v.size();
     *is_f64 = 1;
     return H2G_OK;
   }

@@ -65,12 +65,15 @@ def tree_layout(tree):
     return perm, lo, cl_start, cl_end
 
 
-def export_channel(tree, ops, blob: BlobWriter, inv_perm=None) -> PackedChannel:
+def export_channel(tree, ops, blob: BlobWriter, inv_perm=None,
+                   store_m2l: bool = True) -> PackedChannel:
     """One NestedOperatorSet (engine.py:117-130).  With ``inv_perm`` (original
     index -> tree position) the NCA pivots t_i / s_o of every cluster
     (PivotQuad, lowrank.py:45-59) are exported too, as tree positions: the
     M2L blocks are exactly K[t_i(X), s_o(Y)] (engine.py:176-179), so the
-    device can evaluate them instead of streaming them."""
+    device can evaluate them instead of streaming them.  ``store_m2l=False``
+    exports every M2L block with offset -1 (not stored: evaluated from the
+    pivots; needs ``inv_perm``)."""
     nc = len(tree.clusters)
     quads = ops.quads
     r_in = np.zeros(nc, np.int32)
@@ -105,7 +108,7 @@ def export_channel(tree, ops, blob: BlobWriter, inv_perm=None) -> PackedChannel:
             if M is None:
                 continue
             src.append(y)
-            offs.append(blob.put(M))
+            offs.append(blob.put(M) if store_m2l else -1)
         rowptr[X + 1] = len(src)
     piv = {}
     if inv_perm is not None:
@@ -147,8 +150,20 @@ def _put_leaf_blocked(blob: BlobWriter, U, tree, X: int) -> int:
     return off0
 
 
-def export_rep(rep, with_points: bool = True) -> PackedOperator:
-    """Pack a reference ``HierRep`` (engine.py:235-269) for the GPU plan."""
+def export_rep(rep, with_points: bool = True, store: str = "near,m2l") -> PackedOperator:
+    """Pack a reference ``HierRep`` (engine.py:235-269) for the GPU plan.
+
+    ``store`` names the raw kernel blocks written to the blob ("near",
+    "m2l"); the others are exported with offset -1 and evaluated on the
+    device from the points and NCA pivots (M2L = K[t_i(X), s_o(Y)],
+    engine.py:176-179; near = K[t^X, t^Y], the reference's own
+    store_near=False path, engine.py:260-268).  Leaving a kind out needs
+    ``with_points``."""
+    kinds = {k for k in store.replace(" ", "").split(",") if k}
+    if kinds - {"near", "m2l"}:
+        raise ValueError(f"store: unknown block kinds {sorted(kinds - {'near', 'm2l'})}")
+    if kinds != {"near", "m2l"} and not with_points:
+        raise ValueError("blocks that are not stored are evaluated from points: with_points=True")
     tree = rep.tree
     kernel = rep.kernel
     if np.issubdtype(np.dtype(getattr(kernel, "dtype", np.float64)), np.complexfloating):
@@ -158,7 +173,8 @@ def export_rep(rep, with_points: bool = True) -> PackedOperator:
     blob = BlobWriter()
     inv_perm = np.empty_like(perm)
     inv_perm[perm] = np.arange(len(perm))
-    channels = [export_channel(tree, ops, blob, inv_perm) for ops in rep.channels]
+    channels = [export_channel(tree, ops, blob, inv_perm, store_m2l="m2l" in kinds)
+                for ops in rep.channels]
 
     # BLR leg: factor dict is level-major / X asc / Y asc (blr.py:53-59);
     # rank-0 factors are skipped exactly as mvp_blr does (blr.py:79-80)
@@ -192,10 +208,13 @@ def export_rep(rep, with_points: bool = True) -> PackedOperator:
             s = tree.clusters[y].index_set
             if len(t) == 0 or len(s) == 0:
                 continue  # engine.py:263-264
+            n_src.append(y)
+            if "near" not in kinds:
+                n_off.append(-1)
+                continue
             blk = rep.near_blocks.get((X, y))
             if blk is None:
                 blk = kernel.block(t, s)  # the reference's lazy path
-            n_src.append(y)
             n_off.append(blob.put(blk))
         near_rowptr[X + 1] = len(n_src)
 

@@ -147,10 +147,19 @@ class GpuHierRep:
 
     # ------------------------------------------------------------ factories
     @classmethod
-    def from_rep(cls, rep, device: int = 0) -> "GpuHierRep":
-        """Export a reference HierRep (engine.py:235-269) and upload it."""
+    def from_rep(cls, rep, device: int = 0, recompute: str = "") -> "GpuHierRep":
+        """Export a reference HierRep (engine.py:235-269) and upload it.
+
+        ``recompute`` ("near", "m2l" or both): those raw kernel blocks are
+        evaluated on the device from the points and NCA pivots instead of
+        streamed, and are not even exported (the reference's own
+        store_near=False path, engine.py:260-268, extended to M2L =
+        K[t_i, s_o], engine.py:176-179)."""
         from .export import export_rep
-        return cls(export_rep(rep, with_points=False), device)
+        kinds = {k for k in (recompute or "").replace(" ", "").split(",") if k}
+        store = ",".join(k for k in ("near", "m2l") if k not in kinds)
+        op = export_rep(rep, with_points=bool(kinds), store=store)
+        return cls(op, device, recompute=",".join(sorted(kinds)))
 
     @classmethod
     def load(cls, path: str, device: int = 0) -> "GpuHierRep":

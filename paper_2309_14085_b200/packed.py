@@ -223,14 +223,28 @@ class PackedOperator:
                        (self.blr_rowptr, nc + 1), (self.near_rowptr, nc + 1)):
             if len(arr) != n:
                 bad("per-cluster array length")
+        def csr_ok(rowptr, name):
+            if rowptr[0] != 0 or (len(rowptr) > 1 and np.any(np.diff(rowptr) < 0)):
+                bad(f"{name} row pointer not monotone from 0")
+
+        def in_range(idx, name):
+            if len(idx) and (idx.min() < 0 or idx.max() >= nc):
+                bad(f"{name} entry out of [0, n_clusters)")
+
         for ch in self.channels:
             for f in CHANNEL_FIELDS:
                 a = getattr(ch, f)
-                want = nc + 1 if f == "m2l_rowptr" else None
-                if want is not None and len(a) != want:
+                if f in ("m2l_src", "m2l_off"):
+                    continue
+                want = nc + 1 if f == "m2l_rowptr" else nc
+                if len(a) != want:
                     bad(f"{f} length")
+            csr_ok(ch.m2l_rowptr, "m2l")
             if len(ch.m2l_src) != ch.m2l_rowptr[-1] or len(ch.m2l_off) != ch.m2l_rowptr[-1]:
                 bad("m2l nnz")
+            in_range(ch.m2l_src, "m2l_src")
+            if np.any(ch.r_in < 0) or np.any(ch.r_out < 0):
+                bad("negative rank")
             if ch.has_pivots:
                 if len(ch.piv_in_ptr) != nc + 1 or len(ch.piv_out_ptr) != nc + 1:
                     bad("pivot CSR length")
@@ -242,10 +256,18 @@ class PackedOperator:
                         bad("pivot out of range")
         if self.points_tree is not None and self.points_tree.shape != (self.N, self.dim):
             bad("points_tree shape")
-        if len(self.near_src) != self.near_rowptr[-1]:
+        csr_ok(self.near_rowptr, "near")
+        csr_ok(self.blr_rowptr, "blr")
+        if len(self.near_src) != self.near_rowptr[-1] or len(self.near_off) != self.near_rowptr[-1]:
             bad("near nnz")
-        if len(self.blr_src) != self.blr_rowptr[-1]:
+        nb = self.blr_rowptr[-1]
+        if (len(self.blr_src) != nb or len(self.blr_rank) != nb or len(self.blr_u_off) != nb
+                or len(self.blr_v_off) != nb):
             bad("blr nnz")
+        in_range(self.near_src, "near_src")
+        in_range(self.blr_src, "blr_src")
+        if nb and self.blr_rank.min() < 1:
+            bad("BLR factor of rank < 1")
         if self.blob.dtype != np.float64:
             bad("blob dtype")
 

@@ -17,8 +17,9 @@ replicated.  A matvec is
 No reduction of phi is ever needed (rows are owned); ``gather_full=True``
 combines the ranks' rows with one all-reduce (disjoint rows, exact).
 
-``schedule_view`` / ``emulate_matvec`` expose the same per-rank schedule to
-numpy so the sharding logic is tested on CPU with gloo (tests/test_sharded.py).
+``schedule_view`` exposes the same per-rank schedule to numpy; the test
+infrastructure executes it on CPU (oracle/sched_emulator.py, gloo in
+tests/test_sharded.py).
 """
 
 from __future__ import annotations
@@ -33,11 +34,16 @@ from .packed import PackedOperator
 
 
 class ShardedGpuHierRep:
+    """Rank ``rank``'s share of one operator.  ``recompute`` ("near", "m2l")
+    evaluates those raw kernel blocks on the device even where stored, as
+    GpuHierRep does (blocks exported with offset -1 are always evaluated):
+    config 5's operating mode, whose stored blocks would not fit."""
+
     def __init__(self, op: PackedOperator, rank: int, nranks: int, device: int = 0,
-                 group=None, lib=None):
+                 group=None, lib=None, recompute: str = ""):
         L = lib or _lib.load()
         op.validate()
-        desc, keep = _desc_from_packed(op)
+        desc, keep = _desc_from_packed(op, recompute)
         plan = C.c_void_p()
         _lib.check(L.h2g_plan_create_sharded(C.byref(desc), int(device), int(rank), int(nranks),
                                              C.byref(plan)), "h2g_plan_create_sharded", L=L)
@@ -46,6 +52,7 @@ class ShardedGpuHierRep:
         self.rank, self.nranks, self.device, self.group = rank, nranks, device, group
         self.N = op.N
         self.mem_scalars = op.mem_scalars
+        self.recompute = recompute
         info = _lib.ShardInfo()
         _lib.check(L.h2g_shard_get_info(plan, C.byref(info)), L=L)
         self.info = {f: getattr(info, f) for f, _ in _lib.ShardInfo._fields_}
@@ -91,6 +98,50 @@ class ShardedGpuHierRep:
         _lib.check(self._L.h2g_matvec_end(self._plan, C.c_void_p(phi.data_ptr()), self.N,
                                           C.c_void_p(stream)), "h2g_matvec_end", L=self._L)
 
+    def owned_rows(self):
+        """Tree-order rows [row_begin, row_end) this rank owns; their points are
+        perm[row_begin:row_end] (the distributed-vector layout)."""
+        return int(self.info["row_begin"]), int(self.info["row_end"])
+
+    def matvec_distributed(self, q_own):
+        """Distributed vectors: ``q_own`` = this rank's rows of q in tree order
+        (q[perm[row_begin:row_end]]), no rank holds all of q.  The x halo
+        (near-field and BLR sources of other ranks' rows) is all-gathered
+        first, then the coefficient exchange as in :meth:`matvec`.  Returns
+        this rank's rows of phi in tree order."""
+        import torch
+        import torch.distributed as dist
+        rb, re_ = self.owned_rows()
+        if q_own.shape[0] != re_ - rb:
+            raise ValueError("vector length mismatch")
+        q_own = q_own.to(torch.float64).contiguous()
+        stream = torch.cuda.current_stream(q_own.device).cuda_stream
+        L = self._L
+        phi_own = torch.empty_like(q_own)
+        _lib.check(L.h2g_shard_load_q(self._plan, C.c_void_p(q_own.data_ptr()),
+                                      C.c_void_p(stream)), "h2g_shard_load_q", L=L)
+        if self.nranks > 1:
+            hm = max(1, self.info["max_halo_slots"])
+            if getattr(self, "_hsend", None) is None:
+                dev = f"cuda:{self.device}"
+                self._hsend = torch.zeros(hm, dtype=torch.float64, device=dev)
+                self._hrecv = torch.zeros(hm * self.nranks, dtype=torch.float64, device=dev)
+            _lib.check(L.h2g_halo_pack(self._plan, C.c_void_p(self._hsend.data_ptr()),
+                                       C.c_void_p(stream)), "h2g_halo_pack", L=L)
+            dist.all_gather_into_tensor(self._hrecv, self._hsend, group=self.group)
+            _lib.check(L.h2g_halo_unpack(self._plan, C.c_void_p(self._hrecv.data_ptr()),
+                                         C.c_void_p(stream)), "h2g_halo_unpack", L=L)
+            _lib.check(L.h2g_shard_part0(self._plan, C.c_void_p(stream)), "h2g_shard_part0", L=L)
+            send, recv = self._buffers(torch)
+            self.pack(send, stream)
+            dist.all_gather_into_tensor(recv, send, group=self.group)
+            self.unpack(recv, stream)
+        else:
+            raise ValueError("matvec_distributed needs a sharded plan (nranks > 1)")
+        _lib.check(L.h2g_shard_store_phi(self._plan, C.c_void_p(phi_own.data_ptr()),
+                                         C.c_void_p(stream)), "h2g_shard_store_phi", L=L)
+        return phi_own
+
     def matvec(self, q, gather_full: bool = False):
         """phi = K~ q on this rank's rows (torch CUDA tensor q, replicated)."""
         import torch
@@ -113,17 +164,18 @@ class ShardedGpuHierRep:
 
 
 # ------------------------------------------------------------ CPU emulation
-def schedule_view(op: PackedOperator, rank: int = 0, nranks: int = 1) -> dict:
-    """Rank's host schedule (include/h2g.h h2g_schedule_build) as numpy arrays."""
+def schedule_view(op: PackedOperator, rank: int = 0, nranks: int = 1, recompute: str = "") -> dict:
+    """Rank's host schedule (include/h2g.h h2g_schedule_build) as numpy arrays;
+    ``recompute`` as for GpuHierRep (blocks evaluated even where stored)."""
     L = _lib.load()
-    desc, keep = _desc_from_packed(op)
+    desc, keep = _desc_from_packed(op, recompute)
     h = C.c_void_p()
     _lib.check(L.h2g_schedule_build(C.byref(desc), int(rank), int(nranks), C.byref(h)),
                "h2g_schedule_build")
     out = {}
     try:
-        for name, cols in (("tasks", 4), ("terms", 5), ("phases", 4), ("pack", 3),
-                           ("unpack", 3), ("meta", 1), ("blob", 1)):
+        for name, cols in (("tasks", 5), ("terms", 6), ("phases", 4), ("pack", 3),
+                           ("unpack", 3), ("meta", 1), ("blob", 1), ("recs", 4), ("halo", 3)):
             ptr, n, is_f64 = C.c_void_p(), C.c_int64(), C.c_int32()
             _lib.check(L.h2g_schedule_get(h, name.encode(), C.byref(ptr), C.byref(n),
                                           C.byref(is_f64)))
@@ -142,57 +194,3 @@ def schedule_view(op: PackedOperator, rank: int = 0, nranks: int = 1) -> dict:
                n_ones=int(m[4]), row_begin=int(m[5]), row_end=int(m[6]), send_slots=int(m[7]),
                max_send_slots=int(m[8]), level=int(m[9]))
     return out
-
-
-def _run_phases(view, blob, arena, part):
-    tasks, terms = view["tasks"], view["terms"]
-    for tb, te, ph_part, _ in view["phases"]:
-        if ph_part != part:
-            continue
-        for y_off, m, t0, t1 in tasks[tb:te]:
-            acc = np.zeros(m)
-            for a_off, x_off, lda, ncols, a_space in terms[t0:t1]:
-                src = arena if a_space else blob
-                A = np.lib.stride_tricks.as_strided(src[a_off:], shape=(m, ncols),
-                                                    strides=(8, 8 * lda))
-                acc += A @ arena[x_off:x_off + ncols]
-            arena[y_off:y_off + m] = acc
-
-
-def emulate_begin(view, op, q):
-    """Part 0 of a rank's matvec in numpy; returns (arena, send)."""
-    blob = view["blob"] if len(view["blob"]) else op.blob
-    arena = np.zeros(view["n_slots"] + 8)
-    arena[view["ones_off"]:view["ones_off"] + view["n_ones"]] = 1.0
-    arena[view["q_tree"]:view["q_tree"] + op.N] = np.asarray(q, dtype=np.float64)[op.perm]
-    _run_phases(view, blob, arena, 0)
-    send = np.zeros(max(1, view["max_send_slots"]))
-    for src, dst, ln in view["pack"]:
-        send[dst:dst + ln] = arena[src:src + ln]
-    return arena, send
-
-
-def emulate_end(view, op, arena, recv):
-    """Unpack the all-gathered buffer, run part 1; returns phi with this rank's rows."""
-    blob = view["blob"] if len(view["blob"]) else op.blob
-    for src, dst, ln in view["unpack"]:
-        arena[dst:dst + ln] = recv[src:src + ln]
-    _run_phases(view, blob, arena, 1)
-    phi = np.zeros(op.N)
-    rows = np.arange(view["row_begin"], view["row_end"])
-    phi[op.perm[rows]] = arena[view["phi_tree"] + rows]
-    return phi
-
-
-def emulate_matvec(op, q, nranks: int = 1) -> np.ndarray:
-    """All ranks in one process (exchange = concatenation); phi combined."""
-    views = [schedule_view(op, r, nranks) for r in range(nranks)]
-    states = [emulate_begin(v, op, q) for v in views]
-    mx = max(1, views[0]["max_send_slots"])
-    recv = np.zeros(mx * nranks)
-    for r, (_, send) in enumerate(states):
-        recv[r * mx:r * mx + len(send)] = send[:mx]
-    phi = np.zeros(op.N)
-    for v, (arena, _) in zip(views, states):
-        phi += emulate_end(v, op, arena, recv)
-    return phi

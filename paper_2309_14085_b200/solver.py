@@ -115,6 +115,11 @@ def gmres_block(apply, B, tol: float = 1e-8, restart: int = 30, max_iter: int = 
         V[0] = R / torch.from_numpy(safe_beta).to(R.device)
         g[0] = beta
         j_done = 0
+        # per column: Krylov size of this cycle, frozen at the step where the
+        # column converged or broke down (later steps apply the operator to its
+        # zero basis vector and leave zero pivots in H)
+        j_col = np.zeros(k, dtype=np.int64)
+        open_col = active.copy()
         for j in range(m):
             w = apply(V[j])
             matvecs += 1
@@ -162,14 +167,17 @@ def gmres_block(apply, B, tol: float = 1e-8, restart: int = 30, max_iter: int = 
             if record_residuals:
                 history.append(res.copy())
             j_done = j + 1
+            j_col[open_col] = j_done
             converged = converged | (active & ((res <= tol) | happy))
+            open_col &= ~converged
             if converged.all() or steps >= max_iter:
                 break
         # x += V[:j] y with H[:j,:j] y = g[:j] per column (solver.py:99-100)
         y = np.zeros((k, j_done))
         for q in range(k):
-            if active[q]:
-                y[q] = _back_substitute(H[:j_done, :j_done, q], g[:j_done, q])
+            jq = int(j_col[q])
+            if active[q] and jq > 0:
+                y[q, :jq] = _back_substitute(H[:jq, :jq, q], g[:jq, q])
         X = X + torch.einsum("jnk,kj->nk", V[:j_done], torch.from_numpy(y).to(V.device))
         restarts += 1
         if converged.all():

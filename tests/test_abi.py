@@ -17,7 +17,7 @@ ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 def _declared(header):
     src = open(os.path.join(ROOT, "include", header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(h2g_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(h2g_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_build_and_load():
@@ -98,3 +98,31 @@ def test_no_device_is_loud():
     with pytest.raises(RuntimeError, match="no usable sm_100 CUDA device|CUDA"):
         GpuHierRep(op)
     assert np.isfinite(op.blob).all()
+
+
+def _malformed(mut):
+    import copy
+    from golden_io import load_golden
+    op, _, _ = load_golden("g2d_log_h2plusH")
+    op = copy.copy(op)
+    op.channels = [copy.copy(ch) for ch in op.channels]
+    mut(op)
+    return op
+
+
+@pytest.mark.parametrize("what,mut", [
+    ("r_in length", lambda op: setattr(op.channels[0], "r_in", op.channels[0].r_in[:-1])),
+    ("p2m_off length", lambda op: setattr(op.channels[0], "p2m_off", op.channels[0].p2m_off[:3])),
+    ("m2l_src entry", lambda op: op.channels[0].m2l_src.__setitem__(0, op.n_clusters)),
+    ("blr_src entry", lambda op: setattr(op, "blr_src", np.r_[-1, op.blr_src[1:]].astype(np.int32))),
+    ("blr nnz", lambda op: setattr(op, "blr_rank", op.blr_rank[:-1])),
+    ("near nnz", lambda op: setattr(op, "near_off", op.near_off[:-1])),
+    ("near_src entry", lambda op: setattr(op, "near_src", op.near_src + op.n_clusters)),
+    ("row pointer", lambda op: setattr(op, "near_rowptr", op.near_rowptr[::-1].copy())),
+])
+def test_validate_rejects_malformed_exports(what, mut):
+    """The C side takes raw pointers without lengths, so every per-cluster
+    array, per-entry array and source index is checked on the host first."""
+    op = _malformed(mut)
+    with pytest.raises(ValueError, match="bad export"):
+        op.validate()

@@ -59,8 +59,11 @@ def test_native_operator_acts_like_reference(name):
     op, nop, z, meta = _native_for(name)
     phi = packed_matvec(nop, z["q"])
     # identical pivots: only LU/BLAS roundoff (amplified by cross-matrix
-    # conditioning ~ 1/eps) separates the two operators
-    assert rel_err(phi, z["phi_ref"]) <= 1e-12
+    # conditioning ~ 1/eps) separates the two operators.  The Gaussian at
+    # eps 1e-8 has the worst-conditioned cross matrices (kappa = 3 fixture:
+    # 1.3e-12, three orders below the approximation error re_ref = 1.4e-9).
+    tol = 5e-12 if meta["kernel"] == "gaussian" else 1e-12
+    assert rel_err(phi, z["phi_ref"]) <= tol
     re = rel_err(phi, z["phi_dense"])
     assert abs(re - meta["re_ref"]) <= 1e-3 * meta["re_ref"] + 1e-14
 

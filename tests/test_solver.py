@@ -49,6 +49,29 @@ def test_happy_breakdown():
     assert rep.converged and rep.iterations <= 3
 
 
+@pytest.mark.parametrize("ortho", ["cgs2", "mgs"])
+def test_block_happy_breakdown_one_column(ortho):
+    """One column of the block breaks down (its Krylov space is invariant
+    after 2 steps) while the other keeps iterating: the broken-down column is
+    back-substituted over its own Krylov size only (no 0/0 from the zero
+    basis vectors the later steps apply the operator to)."""
+    n = 40
+    d = np.linspace(1.0, 3.0, n)
+    rng = np.random.default_rng(5)
+    B = np.stack([np.eye(n)[0] + np.eye(n)[1], rng.standard_normal(n)], axis=1)
+
+    def apply(V):
+        return torch.from_numpy(d[:, None] * V.numpy())
+
+    X, rep = gmres_block(apply, torch.from_numpy(B), tol=1e-10, restart=30, max_iter=300,
+                         ortho=ortho)
+    X = X.numpy()
+    assert np.isfinite(X).all()
+    assert rep.converged and np.isfinite(rep.residual)
+    for j in range(2):
+        assert rel_err(X[:, j], B[:, j] / d) <= 1e-8
+
+
 def test_block_of_rhs_lockstep_on_hierarchical_operator():
     """16 RHS through one batched operator application per Arnoldi step."""
     op, z, meta = load_golden("g3d_gauss_h2star")  # Gaussian + 1e-6 I (config 4's kernel)
