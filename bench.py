@@ -1,30 +1,40 @@
-"""Benchmark: H2* / (H2+H)* matvec on B200 (BASELINE.json configs[1]).
+"""Benchmark: H2* matvec on B200 (BASELINE.json configs[2], the north-star
+HBM-roofline config).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2] [--variants h2star-bt,h2plusH-star]
+                    [--config cfg3] [--variants h2star-bt] [--recompute auto]
 
-Workload (configs[1]): 2D, N = 1,048,576 points i.i.d. uniform in [-1,1]^2
-(seed 42, reference bench.py:41), K(x,y) = log|x-y| (Log2D, kernels.py:63-71),
-quadtree leaf <= 64, NCA tolerance 1e-8, single RHS q ~ N(0,1) (seed 43).  The
-operator is built on the box by the native builder (libh2b.so), which
-restates the reference construction (identical ranks/pivots on every golden
-case); the reference's own Python build is infeasible here (~30 min).
+Workload (configs[2]): 3D, N = 1,048,576 points i.i.d. uniform in [-1,1]^3
+(seed 42, reference bench.py:41), K(x,y) = 1/|x-y| (InverseR,
+kernels.py:74-81), octree leaf <= 64, NCA tolerance 1e-6, H2*(b+t), single
+RHS q ~ N(0,1) (seed 43).  The operator (89.8 GB, every block stored) is
+built on the box by the native builder (libh2b.so), which restates the
+reference construction (identical trees, ranks and pivots on every golden
+fixture); the reference's own Python build is infeasible at this size.
 
 A step is one matvec phi = K~ q.  ``value`` = matvecs/s of the headline
-variant (h2star-bt) over all ranks, device-timed with CUDA events on the
-plan's stream, inputs resident in HBM; the operator (6.6 GB) is far larger
-than L2 (126 MB), so no flush is needed.  ``e2e`` is the same metric through
-the public API (GpuHierRep.matvec(q, out=phi) on pinned host vectors: H2D
-copy, matvec, D2H copy inside the timed region).  ``roofline`` reports the streaming GEMV
-kernel's achieved algorithmic bytes/s against MEASURED_PEAKS.json.
-``cpu_baseline`` times the oracle port of the reference matvec
-(oracle/packed_matvec.py, one core) on a bounded sample.
+variant in the evaluation mode ``--recompute auto`` picks (cfg 3: the M2L
+blocks K[t_i, s_o] evaluated on the fp64 pipe, everything else streamed),
+device-timed with CUDA events on the plan's stream, inputs resident in HBM;
+the operator is far larger than L2 (126 MB), so no flush is needed.  ``e2e``
+is the same metric through the public API (GpuHierRep.matvec(q, out=phi) on
+pinned host vectors: H2D copy, matvec, D2H copy inside the timed region);
+``e2e.reference_call_shape`` is GpuHierRep.matvec(q) on a pageable numpy q
+returning a fresh phi (the reference's own call shape).  ``roofline``:
+achieved = (8 S + 16 N) / step time (SURVEY §8(d), S = rep.mem_scalars)
+against MEASURED_PEAKS.json; with evaluated blocks that rate is
+"stored-equivalent" and the DRAM traffic / fp64-pipe figures say what bounds
+the step.  ``variants.streamed`` is the same operator with every block read
+from HBM (the pure HBM fraction).  ``cpu_baseline`` times the oracle port of
+the reference matvec (oracle/cpu_reference.py, one core) on a bounded
+sample (full upward pass + one 1/64 subtree's downward pass, extrapolated).
 
---impl reference times that CPU port as the reference arm (rank 0 only).
-Multi-GPU (N > 1, torchrun, NCCL): the operator is sharded by subtrees
-(ShardedGpuHierRep): each rank holds and streams its share and
-one NCCL all-gather exchanges the multipole coefficients per matvec; the same
-problem on more GPUs (strong scaling), time = max over ranks.
+--impl reference times that CPU port as the reference arm (rank 0 only) on
+an operator exported by a separate build process (no repo .so in the timing
+process).  Multi-GPU (N > 1, torchrun, NCCL): the operator is sharded by
+subtrees (ShardedGpuHierRep) with the same evaluation policy;
+one NCCL all-gather exchanges the multipole coefficients per matvec; the
+same problem on more GPUs (strong scaling), time = max over ranks.
 """
 
 from __future__ import annotations
@@ -153,7 +163,11 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def build_op(cfg, variant, n_threads=0):
+DEFAULT_VARIANTS = {"cfg1": "h2star-bt,h2plusH-star", "cfg2": "h2star-bt,h2plusH-star",
+                    "cfg3": "h2star-bt", "cfg4s": "h2star-bt", "cfg5s": "h2star-bt"}
+
+
+def build_op(cfg, variant, n_threads=0, store=None):
     from paper_2309_14085_b200.builder import build_variant, jittered_grid, uniform_points
     if "grid" in cfg:
         pts = jittered_grid(cfg["grid"], cfg["d"], 42)
@@ -161,20 +175,35 @@ def build_op(cfg, variant, n_threads=0):
         pts = uniform_points(cfg["N"], cfg["d"], 42)
     t0 = time.perf_counter()
     op = build_variant(variant, pts, cfg["kernel"], cfg["n_max"], cfg["eps"], n_threads=n_threads,
-                       store=cfg.get("store", "near,m2l"))
+                       store=cfg.get("store", "near,m2l") if store is None else store)
     return op, time.perf_counter() - t0
 
 
+def config_dict(cfg, variant, N, kappa, mem_scalars, world):
+    """The workload (identical in both arms)."""
+    return {"workload": cfg["desc"], "variant": variant, "N": int(N), "kappa": int(kappa),
+            "mem_scalars": int(mem_scalars), "alg_bytes": int(8 * mem_scalars + 16 * N),
+            "parallelism": f"subtree-sharded x{world}" if world > 1 else "single",
+            "l2": "operator > L2 (no flush)"}
+
+
+def export_for_reference(cfg_name, variant, path, n_threads):
+    """Separate build process: the native builder writes the operator's
+    transfer operators, pivots and points (store="": no raw kernel block) to
+    ``path``; the reference arm then loads it without mapping any repo .so."""
+    code = ("import sys, json, time; sys.path.insert(0, %r); import bench; "
+            "cfg = bench.CONFIGS[%r]; op, tb = bench.build_op(cfg, %r, %d, store=''); "
+            "op.save(%r); print(json.dumps({'build_s': tb}))"
+            % (ROOT, cfg_name, variant, n_threads, path))
+    out = subprocess.run([sys.executable, "-c", code], check=True, capture_output=True, text=True)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
 def cpu_port_time(op, q, budget_s=15.0, max_steps=20):
-    """Oracle port of HierRep.matvec (engine.py:250-269), one core."""
-    from oracle.packed_matvec import packed_matvec
-    times = []
-    t_start = time.perf_counter()
-    while len(times) < max_steps and (time.perf_counter() - t_start) < budget_s:
-        t0 = time.perf_counter()
-        packed_matvec(op, q)
-        times.append(time.perf_counter() - t0)
-    return float(np.mean(times)), len(times)
+    """Oracle port of HierRep.matvec (engine.py:250-269), one core, on the
+    bounded sample of oracle/cpu_reference.py."""
+    from oracle.cpu_reference import time_sampled_matvec
+    return time_sampled_matvec(op, q, steps=max_steps, warmup=0, budget_s=budget_s)
 
 
 def recompute_for(cfg, arg, op=None):
@@ -264,19 +293,9 @@ def bench_gmres(rep, op, torch, dev, k=16, restart=30, max_iter=300):
                     "tests/golden/gmres_gauss_ref.npz)"}
 
 
-def bench_variant(op, args, torch, dev, rank, world, recompute=""):
-    from paper_2309_14085_b200.gpu_rep import GpuHierRep
-    rep = GpuHierRep(op, device=dev, recompute=recompute)
-    N = op.N
-    q = np.random.default_rng(43).standard_normal(N)
-    qd = torch.from_numpy(q).to(f"cuda:{dev}")
-    out = torch.empty_like(qd)
-    stream = torch.cuda.Stream(device=dev)
-    L, plan = rep._L, rep._plan
-
-    def step():
-        L.h2g_matvec(plan, qd.data_ptr(), out.data_ptr(), N, 1, 1, stream.cuda_stream)
-
+def _time_steps(step, args, torch, dev, stream, world):
+    """W warm-ups, then K steps between CUDA events on ``stream`` (clocks
+    sampled throughout), max over ranks."""
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -296,51 +315,61 @@ def bench_variant(op, args, torch, dev, rank, world, recompute=""):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
         torch.distributed.barrier()
-    # per-phase CUDA-event timing on the plan stream (roofline of the GEMV kernel)
+    return ms, clk.summary()
+
+
+def bench_variant(op, args, torch, dev, rank, world, recompute="", e2e=True):
+    from paper_2309_14085_b200.gpu_rep import GpuHierRep
+    rep = GpuHierRep(op, device=dev, recompute=recompute)
+    N = op.N
+    q = np.random.default_rng(43).standard_normal(N)
+    qd = torch.from_numpy(q).to(f"cuda:{dev}")
+    out = torch.empty_like(qd)
+    stream = torch.cuda.Stream(device=dev)
+    L, plan = rep._L, rep._plan
+
+    def step():
+        L.h2g_matvec(plan, qd.data_ptr(), out.data_ptr(), N, 1, 1, stream.cuda_stream)
+
+    ms, clk = _time_steps(step, args, torch, dev, stream, world)
+    # per-phase CUDA-event timing on the plan stream (which phase dominates)
     prof = rep.profile_phases(qd, out, iters=max(3, min(args.steps, 10)))
-    # e2e through the public API with pinned host buffers
+    res = {"rep": rep, "ms": ms, "prof": prof, "clk": clk, "q": q, "out": out}
+    if args.nrhs > 1 and not recompute:
+        res["multi_rhs"] = bench_multi_rhs(rep, op, torch, dev, k=args.nrhs)
+    if not e2e:
+        return res
+    # e2e through the public API with pinned host buffers (out=)
     q_pin = torch.from_numpy(q).pin_memory()
     qh = q_pin.numpy()
     phi_pin = torch.empty(N, dtype=torch.float64).pin_memory().numpy()
-    phi = None
     for _ in range(max(1, args.warmup // 2)):
-        phi = rep.matvec(qh, out=phi_pin)
+        rep.matvec(qh, out=phi_pin)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        phi = rep.matvec(qh, out=phi_pin)
-    e2e_s = (time.perf_counter() - t0) / args.steps
-    res = {"rep": rep, "ms": ms, "prof": prof, "clk": clk.summary(), "e2e_s": e2e_s,
-           "q": q, "phi": phi, "out": out}
-    if args.nrhs > 1 and not recompute:
-        res["multi_rhs"] = bench_multi_rhs(rep, op, torch, dev, k=args.nrhs)
+        rep.matvec(qh, out=phi_pin)
+    res["e2e_s"] = (time.perf_counter() - t0) / args.steps
+    # the reference's call shape: pageable numpy q, freshly allocated phi
+    qp = np.array(q)
+    rep.matvec(qp)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        rep.matvec(qp)
+    res["e2e_ref_shape_s"] = (time.perf_counter() - t0) / args.steps
     if op.kernel.get("name") == "gaussian" and not recompute:
         res["gmres"] = bench_gmres(rep, op, torch, dev, k=max(args.nrhs, 1))
     return res
 
 
-def bench_variant_sharded(op, args, torch, dev, rank, world):
+def bench_variant_sharded(op, args, torch, dev, rank, world, recompute=""):
     """Strong scaling: the operator split over `world` GPUs, one all-gather."""
     from paper_2309_14085_b200.sharded import ShardedGpuHierRep
-    rep = ShardedGpuHierRep(op, rank, world, device=dev)
+    rep = ShardedGpuHierRep(op, rank, world, device=dev, recompute=recompute)
     N = op.N
     q = np.random.default_rng(43).standard_normal(N)
     qd = torch.from_numpy(q).to(f"cuda:{dev}")
-    for _ in range(args.warmup):
-        rep.matvec(qd)
-    torch.cuda.synchronize(dev)
-    torch.distributed.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
-        torch.cuda.synchronize(dev)
-        ev0.record()
-        for _ in range(args.steps):
-            rep.matvec(qd)
-        ev1.record()
-        torch.cuda.synchronize(dev)
-    ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms], device=f"cuda:{dev}")
-    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms = float(t.item())
+    stream = torch.cuda.current_stream(dev)
+    ms, clk = _time_steps(lambda: rep.matvec(qd), args, torch, dev, stream, world)
     # e2e: pinned host q -> device, sharded matvec, this rank's rows -> host
     q_pin = torch.from_numpy(q).pin_memory()
     phi_pin = torch.empty(N, dtype=torch.float64).pin_memory()
@@ -353,64 +382,80 @@ def bench_variant_sharded(op, args, torch, dev, rank, world):
     e2e = torch.tensor([(time.perf_counter() - t0) / args.steps], device=f"cuda:{dev}")
     torch.distributed.all_reduce(e2e, op=torch.distributed.ReduceOp.MAX)
     torch.distributed.barrier()
-    return {"rep": rep, "ms": ms, "prof": [], "clk": clk.summary(), "e2e_s": float(e2e.item()),
+    return {"rep": rep, "ms": ms, "prof": [], "clk": clk, "e2e_s": float(e2e.item()),
             "q": q, "shard": rep.info}
+
+
+def _profile_json(name):
+    path = os.path.join(ROOT, "profiles", name)
+    try:
+        with open(path) as fh:
+            return json.load(fh), os.path.relpath(path, ROOT)
+    except Exception:
+        return None, None
+
+
+def reference_arm(args, cfg, variants, world):
+    """--impl reference: the oracle port of the reference matvec on the box's
+    host (rank 0), on an operator a SEPARATE build process exported (so this
+    process never maps a repo .so), same config / warmup as our arm."""
+    import tempfile
+    n_threads = os.cpu_count() or 1
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "op.npz")
+        info = export_for_reference(args.config, variants[0], path, n_threads)
+        from paper_2309_14085_b200.packed import PackedOperator
+        op = PackedOperator.load(path)
+    q = np.random.default_rng(43).standard_normal(cfg["N"])
+    from oracle.cpu_reference import time_sampled_matvec
+    r = time_sampled_matvec(op, q, steps=args.steps, warmup=args.warmup, budget_s=args.ref_budget)
+    v = r["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "matvec/s",
+            "n_gpus": world, "steps": r["steps"], "warmup": args.warmup,
+            "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (uniform_points seed 42, q ~ N(0,1) seed 43)",
+            "config": config_dict(cfg, variants[0], op.N, op.kappa, op.mem_scalars, world),
+            "operator_source": ("native build in a separate process (libh2b.so), exported with "
+                                "store='' (transfer operators + NCA pivots + points; identical "
+                                "trees, ranks and pivots to the reference build); this process "
+                                f"maps no repo .so; export build {info['build_s']:.1f} s"),
+            "cpu_baseline": {"value": v, "unit": "matvec/s", "cores": 1, "kind": "port",
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": "matvec/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "timing": {k: r[k] for k in ("t_up_s", "t_down_sample_s", "sampled_leaves", "leaves")}}
+    print(json.dumps(line), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--variants", default="h2star-bt,h2plusH-star")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--variants", default=None, help="default: per config (cfg3: h2star-bt)")
+    ap.add_argument("--cpu-budget", type=float, default=60.0)
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="--impl reference: stop timing after this many seconds")
     ap.add_argument("--recompute", default="auto",
                     help="raw kernel blocks evaluated on the device: auto|none|near|m2l|near,m2l")
+    ap.add_argument("--streamed-variant", type=int, default=1,
+                    help="also time the all-streamed plan (pure HBM fraction) when the headline "
+                         "evaluates blocks")
     ap.add_argument("--nrhs", type=int, default=16,
                     help="also time the batched-RHS engine with this many right-hand sides")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
-    variants = [v for v in args.variants.split(",") if v]
+    variants = [v for v in (args.variants or DEFAULT_VARIANTS[args.config]).split(",") if v]
     rank, world, local = dist_env()
     n_threads = max(1, (os.cpu_count() or 1) // max(1, world))
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        op, tb = build_op(cfg, variants[0], n_threads=os.cpu_count() or 1)
-        q = np.random.default_rng(43).standard_normal(cfg["N"])
-        from oracle.packed_matvec import packed_matvec
-        for _ in range(min(args.warmup, 1)):
-            packed_matvec(op, q)
-        budget = 240.0
-        times = []
-        t_all = time.perf_counter()
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            packed_matvec(op, q)
-            times.append(time.perf_counter() - t0)
-            if time.perf_counter() - t_all > budget:
-                break
-        s = float(np.mean(times))
-        v = 1.0 / s
-        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "matvec/s",
-                "n_gpus": args.gpus, "steps": len(times), "warmup": min(args.warmup, 1),
-                "ms_per_step": s * 1e3, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": cfg["desc"], "variant": variants[0], "N": cfg["N"],
-                           "mem_scalars": int(op.mem_scalars),
-                           "operator": "native build (libh2b.so), identical structure/ranks "
-                                       "to the reference build"},
-                "cpu_baseline": {"value": v, "unit": "matvec/s", "cores": 1, "kind": "port",
-                                 "sample": f"{len(times)} full matvecs of the oracle port "
-                                           "(oracle/packed_matvec.py: reference loop structure, "
-                                           "numpy @ per block, OPENBLAS_NUM_THREADS=1)"},
-                "e2e": {"value": v, "unit": "matvec/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        if rank == 0:
+            reference_arm(args, cfg, variants, world)
         return
 
     import torch
@@ -422,110 +467,134 @@ def main():
     results = {}
     for v in variants:
         op, tb = build_op(cfg, v, n_threads=n_threads)
+        rc = recompute_for(cfg, args.recompute, op)
         if world > 1:
-            r = bench_variant_sharded(op, args, torch, dev, rank, world)
+            r = bench_variant_sharded(op, args, torch, dev, rank, world, recompute=rc)
         else:
-            r = bench_variant(op, args, torch, dev, rank, world,
-                              recompute=recompute_for(cfg, args.recompute, op))
-        r["op"] = op
-        r["build_s"] = tb
+            r = bench_variant(op, args, torch, dev, rank, world, recompute=rc)
+        r["op"], r["build_s"], r["rc"] = op, tb, rc
+        if v == variants[0] and rc and world == 1 and args.streamed_variant and cfg.get("store") != "":
+            # the same operator with every block read from HBM: the pure HBM roofline
+            s = bench_variant(op, args, torch, dev, rank, world, recompute="", e2e=False)
+            s["rep"].close()
+            r["streamed"] = s
         results[v] = r
         if v != variants[0]:
             r["rep"].close()
 
     head = variants[0]
     R = results[head]
-    op, rep = R["op"], R["rep"]
-    alg_bytes = 8 * op.mem_scalars + 16 * op.N
+    op, rep, rc = R["op"], R["rep"], R["rc"]
+    S, N = int(op.mem_scalars), int(op.N)
+    alg_bytes = 8 * S + 16 * N
     value = 1e3 / R["ms"]  # whole-job matvecs/s (one operator, sharded over `world` GPUs)
     peak, peak_src = _peaks()
+
+    def span_ms(r):  # the GEMV/P2P launches between the gather and scatter kernels
+        edge = sum(p["ms"] for p in r["prof"] if p["phase"] in ("gather", "scatter"))
+        return max(r["ms"] - edge, 1e-9)
+
+    achieved = alg_bytes / world / (R["ms"] * 1e-3) / 1e9  # per GPU
+    roof = {"bound": "fp64+hbm" if rc else "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+            "achieved_basis": "(8 S + 16 N) / step time, S = rep.mem_scalars (SURVEY §8(d))"
+                              + (" per GPU" if world > 1 else "")}
     if world == 1:
-        # roofline: streaming GEMV kernel phases (algorithmic bytes / event time)
-        gemv = [p for p in R["prof"] if p["phase"] not in ("gather", "scatter", "blr_reduce")]
-        rc = recompute_for(cfg, args.recompute, op)
-        k_bytes = sum(p["bytes"] for p in gemv)
-        k_ms_serial = sum(p["ms"] for p in gemv)
-        # the GEMV launches overlap at phase boundaries (programmatic dependent
-        # launch), so their average duration is their span inside the timed
-        # step: step time minus the gather / scatter kernels (event-timed)
-        edge_ms = sum(p["ms"] for p in R["prof"] if p["phase"] in ("gather", "scatter"))
-        k_ms = max(R["ms"] - edge_ms, 1e-9)
-        achieved = k_bytes / (k_ms * 1e-3) / 1e9
-        achieved_serial = k_bytes / (k_ms_serial * 1e-3) / 1e9
-        dom = max(gemv, key=lambda p: p["ms"])
-        dom = {"name": dom["phase"], "ms": dom["ms"],
-               "GBps": dom["bytes"] / (dom["ms"] * 1e-3) / 1e9}
-        kernel = ("stream_gemv_kernel (all GEMV phases)" if not rc else
-                  f"stream_gemv_kernel + p2p_tasks_kernel (all phases; {rc} blocks evaluated "
-                  "on the fp64 pipe: achieved = stored-representation bytes / time, may "
-                  "exceed the HBM peak)")
-    else:
-        # per-GPU share of the algorithmic bytes over the whole (max-over-ranks) step
-        achieved = alg_bytes / world / (R["ms"] * 1e-3) / 1e9
-        achieved_serial = None
-        dom = None
-        kernel = "whole sharded matvec per GPU (all phases + NCCL all-gather)"
-    traffic = None
-    rc_used = recompute_for(cfg, args.recompute, op) if world == 1 else ""
-    tpath = os.path.join(ROOT, "profiles",
-                         f"traffic_{args.config}_{head}{'_eval' if rc_used else ''}.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+        roof["kernel_span_achieved"] = 8 * S / (span_ms(R) * 1e-3) / 1e9
+        roof["kernel_span_frac"] = roof["kernel_span_achieved"] / peak
+        roof["launches_per_step"] = rep.launches_per_matvec() - 2
+        p2p_ms = sum(p["ms"] for p in R["prof"] if _is_p2p_phase(p["phase"], rc))
+        tot_ms = sum(p["ms"] for p in R["prof"]) or 1.0
+        dom = max((p for p in R["prof"] if p["phase"] not in ("gather", "scatter")),
+                  key=lambda p: p["ms"])
+        roof["dominant_phase"] = {"name": dom["phase"], "ms": dom["ms"],
+                                  "engine": "p2p_tasks_kernel" if _is_p2p_phase(dom["phase"], rc)
+                                  else "stream_gemv_kernel"}
+        roof["kernel_share"] = {"p2p_tasks_kernel": p2p_ms / tot_ms,
+                                "stream_gemv_kernel": 1.0 - p2p_ms / tot_ms}
+        if rc:
+            roof["note"] = (f"{rc} blocks are evaluated on the fp64 pipe, never read: achieved is "
+                            "the stored-equivalent rate and may exceed the HBM peak; dram_frac "
+                            "(ncu DRAM bytes of the timed build / step time / peak) is the HBM "
+                            "utilisation and fp64_pipe_frac the P2P kernel's fp64-pipe "
+                            "utilisation (ncu)")
+    tname = f"traffic_{args.config}_{head}{'_eval' if rc else ''}.json"
+    tj, tsrc = _profile_json(tname)
+    roof["traffic"] = tj.get("dram_bytes_per_launch") if tj else None
+    if tj and world == 1:
+        roof["traffic_source"] = tsrc
+        roof["dram_frac"] = roof["traffic"] / (R["ms"] * 1e-3) / 1e9 / peak
+    pj, psrc = _profile_json(f"p2p_{args.config}_{head}.json")
+    if rc and pj and world == 1:
+        roof["fp64_pipe_frac"] = pj.get("fp64_pipe_frac")
+        roof["fp64_source"] = psrc
     line = {
         "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": R["ms"],
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (uniform_points seed 42, q ~ N(0,1) seed 43)",
-        "config": {"workload": cfg["desc"], "variant": head, "N": op.N, "kappa": op.kappa,
-                   "mem_scalars": int(op.mem_scalars), "alg_bytes": alg_bytes,
-                   "parallelism": f"subtree-sharded x{world}" if world > 1 else "single",
-                   "l2": "operator > L2 (no flush)", "build_s": round(R["build_s"], 2),
-                   "evaluated_blocks": recompute_for(cfg, args.recompute, op) or "none"},
+        "config": config_dict(cfg, head, N, op.kappa, S, world),
+        "evaluated_blocks": rc or "none", "build_s": round(R["build_s"], 2),
         "achieved_GBps": alg_bytes / (R["ms"] * 1e-3) / 1e9,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "launches_per_step": (rep.launches_per_matvec() - 2) if world == 1 else None,
-                     "achieved_phase_by_phase": achieved_serial if world == 1 else None,
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": kernel, "dominant_phase": dom},
+        "roofline": roof,
         "e2e": {"value": 1.0 / R["e2e_s"], "unit": "matvec/s",
-                "h2d_bytes_per_step": 8 * op.N, "d2h_bytes_per_step": 8 * op.N},
+                "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N},
         "gpu_launches": args.steps * rep.launches_per_matvec(),
         "clocks": R["clk"],
         "phases_us": {p["phase"]: round(p["ms"] * 1e3, 1) for p in R["prof"]},
     }
+    if "e2e_ref_shape_s" in R:
+        line["e2e"]["reference_call_shape"] = {
+            "value": 1.0 / R["e2e_ref_shape_s"], "unit": "matvec/s",
+            "call": "GpuHierRep.matvec(q) on a pageable numpy q, fresh phi (engine.py:250-269)"}
+        line["e2e"]["call"] = "GpuHierRep.matvec(q, out=phi) on pinned host buffers"
     if world > 1:
         line["shard"] = R["shard"]
-    if "multi_rhs" in R:
-        line["multi_rhs"] = R["multi_rhs"]
-    if "gmres" in R:
-        line["gmres"] = R["gmres"]
+    for key in ("multi_rhs", "gmres"):
+        if key in R:
+            line[key] = R[key]
     others = {}
+    if "streamed" in R:
+        st = R["streamed"]
+        others["streamed"] = {
+            "evaluated_blocks": "none", "ms_per_step": st["ms"], "matvec_per_s": 1e3 / st["ms"],
+            "hbm_achieved_GBps": alg_bytes / (st["ms"] * 1e-3) / 1e9,
+            "hbm_frac": alg_bytes / (st["ms"] * 1e-3) / 1e9 / peak,
+            "kernel_span_frac": 8 * S / (span_ms(st) * 1e-3) / 1e9 / peak,
+            "clocks": st["clk"],
+            "phases_us": {p["phase"]: round(p["ms"] * 1e3, 1) for p in st["prof"]}}
+        tj2, tsrc2 = _profile_json(f"traffic_{args.config}_{head}.json")
+        if tj2:
+            others["streamed"]["traffic"] = tj2.get("dram_bytes_per_launch")
+        if "multi_rhs" in st:
+            others["streamed"]["multi_rhs"] = st["multi_rhs"]
     for v in variants[1:]:
         r = results[v]
+        b = 8 * r["op"].mem_scalars + 16 * r["op"].N
         others[v] = {"ms_per_step": r["ms"], "matvec_per_s": 1e3 / r["ms"],
-                     "mem_scalars": int(r["op"].mem_scalars),
-                     "achieved_GBps": (8 * r["op"].mem_scalars + 16 * r["op"].N) / (r["ms"] * 1e-3) / 1e9,
+                     "mem_scalars": int(r["op"].mem_scalars), "evaluated_blocks": r["rc"] or "none",
+                     "achieved_GBps": b / (r["ms"] * 1e-3) / 1e9, "frac": b / (r["ms"] * 1e-3) / 1e9 / peak,
                      "e2e_matvec_per_s": 1.0 / r["e2e_s"], "build_s": round(r["build_s"], 2)}
     if others:
         line["variants"] = others
-    if rank == 0 and world == 1 and cfg.get("store") == "":
-        line["cpu_baseline"] = {"value": None, "unit": "matvec/s", "cores": 1, "kind": "port",
-                                "sample": "not run: the operator's near/M2L blocks are not stored "
-                                          "and the numpy oracle would evaluate ~10^10 entries"}
-    elif rank == 0 and world == 1:
-        t_cpu, n_cpu = cpu_port_time(op, R["q"], budget_s=args.cpu_budget)
-        line["cpu_baseline"] = {"value": 1.0 / t_cpu, "unit": "matvec/s", "cores": 1, "kind": "port",
-                                "sample": f"{n_cpu} full matvecs of the oracle port on the same "
-                                          "operator (oracle/packed_matvec.py, 1 BLAS thread)"}
+    if rank == 0 and world == 1:
+        t = cpu_port_time(op, R["q"], budget_s=args.cpu_budget, max_steps=1)
+        line["cpu_baseline"] = {"value": t["value"], "unit": "matvec/s", "cores": 1, "kind": "port",
+                                "sample": t["sample"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     rep.close()
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def _is_p2p_phase(name, rc):
+    """Phases the P2P (kernel-evaluation) engine runs under the recompute policy."""
+    if name.endswith("_red"):
+        return False
+    return ("m2l" in (rc or "") and name.startswith("down_l")) or (
+        "near" in (rc or "") and name == "leaf")
 
 
 if __name__ == "__main__":

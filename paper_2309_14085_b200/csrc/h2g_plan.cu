@@ -218,6 +218,9 @@ struct h2g_plan {
   int dim = 2;
   bool has_p2p = false;
   bool pdl = true;  // phases launched with programmatic dependent launch (H2G_PDL=0: off)
+  // upload only the operator blocks the tasks read (sharded plans, and plans
+  // that evaluate stored blocks: the evaluated ones never leave the host)
+  bool compact = false;
   // host-pointer calls on pinned buffers: the whole call (H2D, gather, phases,
   // scatter, D2H) as one cached CUDA graph, keyed by the buffers
   const void* hg_q = nullptr;
@@ -973,7 +976,7 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
   }
   s.phases.back().alg_bytes = bytes;
   end_phase(s);
-  if (sh.nranks == 1 && kPanelize) panelize_tall_blocks(s);
+  if (!p->compact && kPanelize) panelize_tall_blocks(s);
   s.term_r0.clear();
   split_heavy_tasks(s, p->n_slots, ones_off);
   partition_engines(s);
@@ -1500,6 +1503,7 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
   p->mem_scalars = d->mem_scalars;
   HostSchedule s;
   p->shard = make_shard(d, rank, nranks);
+  p->compact = nranks > 1 || d->recompute != 0;
   rc = build_schedule(d, p, s, p->shard);
   if (rc) {
     delete p;
@@ -1519,7 +1523,7 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     p->use_batched = false;  // the tensor-pipe engine streams stored blocks only
   }
   std::vector<double> local_blob;
-  if (nranks > 1) compact_blob(d, s, local_blob);
+  if (p->compact) compact_blob(d, s, local_blob);
   {
     const char* e = getenv("H2G_ENGINE");
     if (e && std::string(e) == "ldg") p->engine = 0;
@@ -1564,7 +1568,7 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
     int r;
-    if (nranks > 1) {
+    if (p->compact) {
       p->blob_len = (int64_t)local_blob.size();
       if ((r = upload((void**)&p->d_blob, local_blob.data(), sizeof(double) * local_blob.size())))
         return r;
@@ -2203,10 +2207,11 @@ int h2g_schedule_build(const h2g_export_desc* desc, int rank, int nranks, h2g_sc
   h2g_plan tmp;
   HostSchedule s;
   tmp.shard = make_shard(desc, rank, nranks);
+  tmp.compact = nranks > 1 || desc->recompute != 0;
   rc = build_schedule(desc, &tmp, s, tmp.shard);
   if (rc) return rc;
   h2g_sched* o = new h2g_sched();
-  if (nranks > 1) compact_blob(desc, s, o->blob);
+  if (tmp.compact) compact_blob(desc, s, o->blob);
   if (!s.panels.empty()) {  // the blob the device holds: tall blocks as row panels
     o->blob.assign(desc->blob, desc->blob + desc->blob_len);
     std::vector<double> pan;

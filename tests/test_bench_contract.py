@@ -53,3 +53,42 @@ def test_configs_match_baseline_shapes(bench):
     assert cfg["cfg3"]["N"] == 1048576 and cfg["cfg3"]["d"] == 3
     for c in cfg.values():
         assert c["n_max"] == 64
+
+
+def test_default_workload_is_cfg3_and_arms_share_config(bench):
+    """The N=1 line is BASELINE configs[2] (the north-star HBM config); both
+    arms build their config dict with the same function and keys."""
+    import sys
+    argv = sys.argv
+    cfg = bench.CONFIGS["cfg3"]
+    assert (cfg["N"], cfg["d"], cfg["kernel"], cfg["eps"]) == (1048576, 3, "lap3d", 1e-6)
+    assert bench.DEFAULT_VARIANTS["cfg3"] == "h2star-bt"
+    a = bench.config_dict(cfg, "h2star-bt", 1048576, 5, 11222271705, 1)
+    b = bench.config_dict(cfg, "h2star-bt", 1048576, 5, 11222271705, 1)
+    assert a == b and a["alg_bytes"] == 8 * 11222271705 + 16 * 1048576
+    assert bench.recompute_for(cfg, "auto") == "m2l"
+    assert bench.recompute_for(cfg, "none") == ""
+    assert bench._is_p2p_phase("down_l5", "m2l") and not bench._is_p2p_phase("leaf", "m2l")
+    assert not bench._is_p2p_phase("down_l3_red", "m2l")
+    sys.argv = argv
+
+
+def test_reference_arm_maps_no_repo_library(tmp_path, bench):
+    """The reference arm's timing process loads an export written by a
+    separate build process and never maps libh2g / libh2b."""
+    import json
+    import subprocess
+    import sys
+    code = (
+        "import sys, json; sys.path.insert(0, %r); import bench, numpy as np;"
+        "info = bench.export_for_reference('cfg1', 'h2star-bt', %r, 2);"
+        "from paper_2309_14085_b200.packed import PackedOperator;"
+        "op = PackedOperator.load(%r);"
+        "from oracle.cpu_reference import time_sampled_matvec;"
+        "r = time_sampled_matvec(op, np.random.default_rng(43).standard_normal(op.N), steps=1);"
+        "maps = open('/proc/self/maps').read();"
+        "print(json.dumps({'v': r['value'], 'so': ('libh2g' in maps) or ('libh2b' in maps)}))"
+        % (ROOT, str(tmp_path / "op.npz"), str(tmp_path / "op.npz")))
+    out = subprocess.run([sys.executable, "-c", code], check=True, capture_output=True, text=True)
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["v"] > 0 and res["so"] is False

@@ -116,3 +116,42 @@ def test_exported_pivots_reproduce_stored_m2l(name):
                                  ch.piv_out[ch.piv_out_ptr[Y]:ch.piv_out_ptr[Y + 1]])
                 worst = max(worst, float(np.max(np.abs(M - K), initial=0.0)))
     assert worst <= 1e-15
+
+
+@pytest.mark.parametrize("name", ["g2d_log_h2star", "g2d_log_h2plusH", "g3d_lap_k3_h2plusH",
+                                  "g2d_cfg1_h2star", "g3d_gauss_k3_h2star"])
+def test_restricted_oracle_equals_full(name):
+    """packed_matvec_rows (the BASELINE-scale oracle on sampled target leaves)
+    reproduces the full restatement's rows and the reference's own phi."""
+    from oracle.packed_matvec import packed_matvec_rows
+    op, z, meta = load_golden(name)
+    lo = op.level_offset
+    leaves = np.random.default_rng(1).choice(np.arange(lo[op.kappa], lo[op.kappa + 1]), 7,
+                                             replace=False)
+    rows, vals = packed_matvec_rows(op, z["q"], leaves)
+    full = packed_matvec(op, z["q"])
+    assert len(rows) == sum(op.size(x) for x in leaves)
+    assert np.max(np.abs(vals - full[rows])) <= 1e-14 * np.max(np.abs(full))
+    assert rel_err(vals, z["phi_ref"][rows]) <= 1e-13
+    rows_ld, vals_ld = packed_matvec_rows(op, z["q"], leaves, dtype=np.longdouble)
+    assert np.array_equal(rows_ld, rows)
+    assert rel_err(vals, vals_ld.astype(np.float64)) <= 1e-13
+
+
+def test_sampled_cpu_reference_timer():
+    """bench.py's CPU reference leg: upward pass + one subtree's downward pass;
+    the sampled rows it computes are the full restatement's."""
+    from oracle.cpu_reference import sample_leaves, time_sampled_matvec
+    from oracle.packed_matvec import downward_rows, upward_pass
+    op, z, meta = load_golden("g3d_lap_k3_h2star")  # compact: blocks evaluated untimed
+    leaves, L = sample_leaves(op, frac_level=2)
+    assert L == 2 and len(leaves) == 8
+    assert len(sample_leaves(op)[0]) == 512  # small tree: the whole matvec
+    r = time_sampled_matvec(op, z["q"], steps=1)
+    assert r["value"] > 0 and r["sampled_leaves"] == 512
+    q_tree = z["q"][op.perm]
+    out = downward_rows(op, q_tree, upward_pass(op, q_tree), leaves)
+    full = packed_matvec(op, z["q"])
+    for x in leaves:
+        rows = op.perm[op.cl_start[x]:op.cl_end[x]]
+        assert np.allclose(out[x], full[rows], rtol=0, atol=1e-13 * np.abs(full).max())
