@@ -208,18 +208,65 @@ void for_blocks(int64_t n, bool par, F f) {
   }
 }
 
+// sum_i a[i] * b[i] over [0, n) with 8 interleaved partial sums (vectorised;
+// fixed order, so independent of the thread count).  The reference's
+// np.vdot / np.linalg.norm are BLAS reductions with their own blocking, so
+// these only enter the Frobenius stopping estimate, never a pivot choice.
+inline double dot8(const double* a, const double* b, int64_t n) {
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8)
+    for (int l = 0; l < 8; ++l) acc[l] += a[i + l] * b[i + l];
+  for (int l = 0; i < n; ++i, ++l) acc[l] += a[i] * b[i];
+  return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
 // sum_i a[i] * b[i] with fixed block partials
 double dot_blocked(const double* a, const double* b, int64_t n, bool par) {
   const int64_t nb = (n + kBlk - 1) / kBlk;
   std::vector<double> part(std::max<int64_t>(nb, 1), 0.0);
   for_blocks(n, par, [&](int64_t blk, int64_t b0, int64_t b1) {
-    double s = 0;
-    for (int64_t i = b0; i < b1; ++i) s += a[i] * b[i];
-    part[blk] = s;
+    part[blk] = dot8(a + b0, b + b0, b1 - b0);
   });
   double s = 0;
   for (int64_t k = 0; k < nb; ++k) s += part[k];
   return s;
+}
+
+// Kernel row K[ri, cols[b0 .. b1)] into out, columns' coordinates gathered
+// contiguously in cp (n x d).  1/r runs as a vector loop (sqrt and division
+// are correctly rounded, so every entry is bitwise the scalar Kernel::entry);
+// r == 0 entries (coincident points, i == j) are fixed up by entry().
+void row_entries(const Kernel& K, int64_t ri, const int64_t* cols, const double* cp, int64_t b0,
+                 int64_t b1, double* out) {
+  const int d = K.d;
+  const double* a = K.pts + ri * d;
+  if (K.type == H2B_KERNEL_LAP3D) {
+    const double a0 = a[0], a1 = d > 1 ? a[1] : 0.0, a2 = d > 2 ? a[2] : 0.0;
+    if (d == 3) {
+      for (int64_t j = b0; j < b1; ++j) {
+        const double t0 = a0 - cp[3 * j], t1 = a1 - cp[3 * j + 1], t2 = a2 - cp[3 * j + 2];
+        double s2 = 0.0;
+        s2 += t0 * t0;
+        s2 += t1 * t1;
+        s2 += t2 * t2;
+        out[j] = 1.0 / std::sqrt(s2);
+      }
+    } else {
+      for (int64_t j = b0; j < b1; ++j) {
+        double s2 = 0.0;
+        for (int k = 0; k < d; ++k) {
+          const double t = a[k] - cp[d * j + k];
+          s2 += t * t;
+        }
+        out[j] = 1.0 / std::sqrt(s2);
+      }
+    }
+    for (int64_t j = b0; j < b1; ++j)
+      if (std::isinf(out[j])) out[j] = K.entry(ri, cols[j]);  // r == 0
+    return;
+  }
+  for (int64_t j = b0; j < b1; ++j) out[j] = K.entry(ri, cols[j]);
 }
 
 // first index of max(mask ? 0 : |v|) (numpy argmax semantics); returns (idx, max)
@@ -256,16 +303,28 @@ AcaOut aca(const Kernel& K, const Idx& rows, const Idx& cols, double eps, bool k
   std::vector<double> row(n), col(m);
   auto& us = out.us;
   auto& vs = out.vs;
+  std::vector<double> cp((size_t)n * K.d);  // column coordinates, contiguous
+  for (int64_t j = 0; j < n; ++j)
+    for (int k = 0; k < K.d; ++k) cp[(size_t)j * K.d + k] = K.pts[cols[j] * K.d + k];
+  const int64_t nblk = (n + kBlk - 1) / kBlk;
+  // per block: <row, row> and <row, v_k> partials, computed while the block's
+  // v_k are still in cache (fused with the residual row)
+  std::vector<double> p_vv(std::max<int64_t>(nblk, 1)), p_cross;
   while (true) {
     // residual row i: K[rows[i], cols] - sum_k u_k[i] v_k (k in order, per entry)
-    for_blocks(n, par, [&](int64_t, int64_t b0, int64_t b1) {
+    const size_t nk = us.size();
+    p_cross.assign((size_t)std::max<int64_t>(nblk, 1) * (nk + 1), 0.0);
+    for_blocks(n, par, [&](int64_t blk, int64_t b0, int64_t b1) {
       const int64_t ri = rows[i];
-      for (int64_t j = b0; j < b1; ++j) row[j] = K.entry(ri, cols[j]);
-      for (size_t k = 0; k < us.size(); ++k) {
+      row_entries(K, ri, cols.data(), cp.data(), b0, b1, row.data());
+      for (size_t k = 0; k < nk; ++k) {
         const double ui = us[k][i];
         const double* v = vs[k].data();
         for (int64_t j = b0; j < b1; ++j) row[j] = row[j] - ui * v[j];
       }
+      p_vv[blk] = dot8(row.data() + b0, row.data() + b0, b1 - b0);
+      for (size_t k = 0; k < nk; ++k)
+        p_cross[(size_t)blk * nk + k] = dot8(row.data() + b0, vs[k].data() + b0, b1 - b0);
     });
     used_rows[i] = 1;
     const auto [jb, mb] = argmax_masked(row.data(), used_cols.data(), n, par);
@@ -294,11 +353,15 @@ AcaOut aca(const Kernel& K, const Idx& rows, const Idx& cols, double eps, bool k
     });
     used_cols[jb] = 1;
     const double nu = std::sqrt(dot_blocked(u.data(), u.data(), m, par));
-    const double nv = std::sqrt(dot_blocked(row.data(), row.data(), n, par));
+    double vv = 0.0;
+    for (int64_t b = 0; b < nblk; ++b) vv += p_vv[b];
+    const double nv = std::sqrt(vv);
     double cross = 0.0;
-    for (size_t k = 0; k < us.size(); ++k)
-      cross += dot_blocked(us[k].data(), u.data(), m, par) *
-               dot_blocked(row.data(), vs[k].data(), n, par);
+    for (size_t k = 0; k < nk; ++k) {
+      double rv = 0.0;
+      for (int64_t b = 0; b < nblk; ++b) rv += p_cross[(size_t)b * nk + k];
+      cross += dot_blocked(us[k].data(), u.data(), m, par) * rv;
+    }
     fro2 += 2.0 * cross + (nu * nv) * (nu * nv);
     us.push_back(std::move(u));
     vs.push_back(row);
@@ -589,7 +652,9 @@ double now();
 template <class F>
 void level_loop(int64_t lo, int64_t hi, F body) {
   const int64_t cnt = hi - lo;
-  if (cnt < 2 * (int64_t)omp_get_max_threads()) {
+  int64_t par_below = 2 * (int64_t)omp_get_max_threads();
+  if (const char* e = getenv("H2B_PAR_BELOW")) par_below = atoll(e);
+  if (cnt < par_below) {
     for (int64_t x = lo; x < hi; ++x) body(x, true);
   } else {
 #pragma omp parallel for schedule(dynamic, 1)

@@ -42,6 +42,12 @@ namespace h2g {
 #endif
 constexpr int kP2PWarps = H2G_P2P_WARPS;  // warps per CTA (one task per CTA)
 constexpr int kP2PCtasPerSm = H2G_P2P_CTAS;
+#ifndef H2G_P2P_HYBRID_CTAS
+#define H2G_P2P_HYBRID_CTAS 2
+#endif
+// P2P CTAs per SM beside one streaming-engine CTA (hybrid phases): 2 x 128
+// threads x 128 registers + 160 x 168 fit the 64K-register file
+constexpr int kP2PHybridCtas = H2G_P2P_HYBRID_CTAS;
 constexpr int kP2PThreads = 32 * kP2PWarps;
 constexpr int kP2PChunk = 32;
 constexpr int kRecompute = 2;  // Term.a_space of a kernel-evaluated block (host schedule)

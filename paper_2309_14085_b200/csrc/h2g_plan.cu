@@ -71,7 +71,12 @@ struct Phase {
   // task_end) on the P2P engine (a phase with kernel-evaluated terms runs
   // wholly there)
   int64_t stream_end = -1;               // -1: all tasks stream
-  int64_t p2p_off = 0;                   // first P2PTask of the phase                    // both engines concurrently (1 stream CTA per SM)
+  int64_t p2p_off = 0;                   // first P2PTask of the phase
+  // HYBRID phase (M2L evaluated with a share of the targets streamed): the
+  // streaming engine (1 CTA per SM) and the P2P engine (kP2PHybridCtas per SM)
+  // run CONCURRENTLY on two graph branches over disjoint targets, so the HBM
+  // and the fp64 pipe are busy at once
+  int32_t hybrid = 0;
 };
 
 // Multi-GPU ownership: subtrees at level `level` are split into
@@ -236,6 +241,9 @@ struct h2g_plan {
   cudaEvent_t ev_done = nullptr;
   cudaStream_t last_stream = nullptr;
   bool ev_pending = false;
+  // hybrid phases: the P2P engine runs on a second branch (fork / join events)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -477,6 +485,7 @@ void split_heavy_tasks(HostSchedule& s, int64_t& slots, int64_t ones_off) {
     phases.push_back(main);
     if (!reduces.empty()) {
       Phase red = ph;
+      red.hybrid = 0;
       red.name = ph.name + "_red";
       red.alg_bytes = 0;
       red.task_begin = (int64_t)tasks.size();
@@ -501,7 +510,13 @@ void partition_engines(HostSchedule& s) {
       ph.stream_end = -1;
       continue;
     }
-    std::vector<Task> st_t, p2p_t(s.tasks.begin() + ph.task_begin, s.tasks.begin() + ph.task_end);
+    std::vector<Task> st_t, p2p_t;
+    if (ph.hybrid) {
+      for (int64_t i = ph.task_begin; i < ph.task_end; ++i)
+        (is_p2p_task(s, s.tasks[i]) ? p2p_t : st_t).push_back(s.tasks[i]);
+    } else {
+      p2p_t.assign(s.tasks.begin() + ph.task_begin, s.tasks.begin() + ph.task_end);
+    }
     auto tcost = [&](const Task& t) {
       int64_t c = 0;
       for (int32_t k = t.t_begin; k < t.t_end; ++k) c += s.terms[k].ncols;
@@ -800,6 +815,12 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
     return fail(H2G_ERR_BAD_EXPORT, "too many point records for int32 indexing");
   double share = d->m2l_recompute_share;
   if (!(share > 0.0 && share < 1.0)) share = 1.0;
+  // hybrid: share of each evaluated level's STORED M2L entries streamed by
+  // whole targets on the streaming engine, concurrently with the evaluation
+  double hyb = 0.0;
+  if (const char* e = getenv("H2G_M2L_STREAM_SHARE")) hyb = atof(e);
+  if (!(hyb > 0.0 && hyb < 1.0)) hyb = 0.0;
+  if (sh.nranks > 1) hyb = 0.0;  // sharded plans: one engine per phase
 
   // ================= part 0: before the exchange =================
   // ---- up_leaf: P2M of every channel ----
@@ -893,19 +914,35 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
     // stored-and-streamed (error diffusion over the level, by entries): the
     // P2P engine then keeps the fp64 pipe and HBM busy at once
     double acc_all = 0.0, acc_rc = 0.0;
+    double h_all = 0.0, h_st = 0.0;  // hybrid: entries seen / streamed by whole targets
+    bool any_streamed_target = false, any_eval_target = false;
     for (int ch = 0; ch < d->n_channels; ++ch) {
       const h2g_channel_desc& c = d->channels[ch];
       for (int64_t x = lo[l]; x < lo[l + 1]; ++x) {
         const int64_t ri = c.r_in[x];
         if (ri == 0 || !mine(x, l)) continue;
         bool rc = false;  // some term of x evaluated
+        bool stream_x = false;  // hybrid: this target's stored blocks all stream
+        if (hyb > 0.0 && (d->recompute & H2G_RECOMPUTE_M2L)) {
+          double e = 0.0;
+          bool all_stored = true;
+          for (int64_t k = c.m2l_rowptr[x]; k < c.m2l_rowptr[x + 1]; ++k) {
+            e += (double)ri * c.r_out[c.m2l_src[k]];
+            all_stored = all_stored && c.m2l_off[k] >= 0;
+          }
+          h_all += e;
+          if (all_stored && e > 0.0 && h_st < hyb * h_all) {
+            stream_x = true;
+            h_st += e;
+          }
+        }
         for (int64_t k = c.m2l_rowptr[x]; k < c.m2l_rowptr[x + 1]; ++k) {
           const int64_t y = c.m2l_src[k];
           if (y < 0 || y >= nc || level_of(y) != l)
             return fail(H2G_ERR_BAD_EXPORT, "m2l source not on the target's level");
           if (c.r_out[y] == 0) continue;
           bool ev = c.m2l_off[k] < 0;
-          if (!ev && (d->recompute & H2G_RECOMPUTE_M2L)) {
+          if (!ev && !stream_x && (d->recompute & H2G_RECOMPUTE_M2L)) {
             const double e = (double)ri * c.r_out[y];
             acc_all += e;
             if (acc_rc < share * acc_all) {
@@ -931,9 +968,11 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
           }
         }
         emit_task(s, u_off[ch][x], ri, bytes, rc ? rin_rec[ch][x] : -1);
+        if (rc) any_eval_target = true; else any_streamed_target = true;
       }
     }
     s.phases.back().alg_bytes = bytes;
+    s.phases.back().hybrid = hyb > 0.0 && any_eval_target && any_streamed_target ? 1 : 0;
     end_phase(s);
   }
 
@@ -998,7 +1037,8 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
   for (Phase& ph : phases) {
     if (ph.kind != PH_GEMV) continue;
     const int64_t nt = stream_end_of(ph) - ph.task_begin;
-    const int n_cta_ph = n_cta;
+    // hybrid phases leave room on every SM for the concurrent P2P CTAs
+    const int n_cta_ph = ph.hybrid && !mma ? std::max(1, n_cta / kCtasPerSm) : n_cta;
     // Batched engine: a wide phase runs in GROUP mode -- G warps share a chunk
     // stream, splitting only its rows (<= 8 tiles each), so tasks never need a
     // cross-warp reduction: G = 1 (m <= 64), 2 (m <= 128), 4; kMmaConsumers / G
@@ -1257,16 +1297,18 @@ cudaError_t launch_k(bool pdl, void (*k)(KArgs...), unsigned grid, unsigned bloc
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
-int launch_p2p(h2g_plan* p, const Phase& ph, int phase_idx, cudaStream_t s) {
+int launch_p2p(h2g_plan* p, const Phase& ph, int phase_idx, cudaStream_t s, bool pdl = true) {
   const int64_t b = stream_end_of(ph), n = ph.task_end - b;
   if (n <= 0) return H2G_OK;
-  const int64_t per_sm = kP2PCtasPerSm;  // one CTA per task, persistent
+  // one CTA per task, persistent; beside the streaming engine's CTA (hybrid
+  // phases) only kP2PHybridCtas fit on an SM
+  const int64_t per_sm = ph.hybrid ? kP2PHybridCtas : kP2PCtasPerSm;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, p->n_sm * per_sm));
   const P2PTask* tk = p->d_p2p_tasks + ph.p2p_off;
   int* ctr = p->d_ctr + 2 * phase_idx;
   const int kt = p->kernel_type, d3 = p->dim >= 3;
 #define H2G_LAUNCH_P2P(KT, DIM)                                                              \
-  CUDA_TRY(launch_k(p->pdl, p2p_tasks_kernel<KT, DIM>, grid, kP2PThreads, 0, s, tk, (int)n,  \
+  CUDA_TRY(launch_k(p->pdl && pdl, p2p_tasks_kernel<KT, DIM>, grid, kP2PThreads, 0, s, tk, (int)n,  \
                     (const Term*)p->d_p2p_terms, (const P2PChunk*)p->d_p2p_chunks,             \
                     (const double4*)p->d_recs4, (const double*)p->d_blob, p->d_arena, p->kp, ctr))
   if (kt == 0) {
@@ -1286,6 +1328,13 @@ int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s, int phase_idx = 0
   if (n <= 0) return H2G_OK;
   const int64_t se = stream_end_of(ph);
   const bool has_stream = se > ph.task_begin, has_p2p = ph.task_end > se;
+  // hybrid phase: the streaming engine on `s`, the P2P engine on the side
+  // branch, concurrently (disjoint outputs); joined before the next phase
+  const bool fork = ph.hybrid && has_stream && has_p2p && p->side;
+  if (fork) {
+    CUDA_TRY(cudaEventRecord(p->ev_fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+  }
   if (has_stream) {
     if (ph.kind == PH_GEMV && p->engine == 1) {
       const size_t smem = kStreamSmem;
@@ -1303,7 +1352,12 @@ int launch_phase(h2g_plan* p, const Phase& ph, cudaStream_t s, int phase_idx = 0
     }
     CUDA_TRY(cudaGetLastError());
   }
-  if (has_p2p) {
+  if (fork) {
+    int rc = launch_p2p(p, ph, phase_idx, p->side, /*pdl=*/false);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(p->ev_join, p->side));
+    CUDA_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
+  } else if (has_p2p) {
     int rc = launch_p2p(p, ph, phase_idx, s);
     if (rc) return rc;
   }
@@ -1357,6 +1411,9 @@ void free_plan(h2g_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
   if (p->ev_done) cudaEventDestroy(p->ev_done);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
+  if (p->side) cudaStreamDestroy(p->side);
   if (p->hg_exec) cudaGraphExecDestroy(p->hg_exec);
   if (p->hg_graph) cudaGraphDestroy(p->hg_graph);
   if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
@@ -1567,6 +1624,13 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
   rc = [&]() -> int {
     CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+    bool any_hybrid = false;
+    for (const Phase& ph : s.phases) any_hybrid = any_hybrid || ph.hybrid;
+    if (any_hybrid) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    }
     int r;
     if (p->compact) {
       p->blob_len = (int64_t)local_blob.size();

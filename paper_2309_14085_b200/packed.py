@@ -37,6 +37,7 @@ Layout (SURVEY.md §8(a')):
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -334,8 +335,27 @@ class PackedOperator:
 
     @classmethod
     def load(cls, path: str) -> "PackedOperator":
+        if os.path.isdir(path):
+            return cls.load_dir(path)
         with np.load(path, allow_pickle=False) as z:
             return cls.from_arrays({k: z[k] for k in z.files})
+
+    def save_dir(self, path: str):
+        """Directory form of the export: one raw ``.npy`` per field, so a
+        multi-GB operator (config 3: 90 GB) is written at disk speed and
+        loaded memory-mapped (:meth:`load_dir`) instead of through a zip."""
+        os.makedirs(path, exist_ok=True)
+        for k, v in self.to_arrays().items():
+            np.save(os.path.join(path, f"{k}.npy"), np.asarray(v), allow_pickle=False)
+
+    @classmethod
+    def load_dir(cls, path: str, mmap: bool = True) -> "PackedOperator":
+        z = {}
+        for f in sorted(os.listdir(path)):
+            if f.endswith(".npy"):
+                z[f[:-4]] = np.load(os.path.join(path, f), mmap_mode="r" if mmap else None,
+                                    allow_pickle=False)
+        return cls.from_arrays(z)
 
 
 class BlobWriter:
