@@ -31,6 +31,7 @@
 
 #include "h2g_eval.cuh"
 #include "h2g_kernels.cuh"
+#include "h2g_stream.cuh"
 
 namespace h2g {
 
@@ -52,16 +53,43 @@ constexpr int kP2PThreads = 32 * kP2PWarps;
 constexpr int kP2PChunk = 32;
 constexpr int kRecompute = 2;  // Term.a_space of a kernel-evaluated block (host schedule)
 constexpr int kSelfBit = 1 << 16;
+#ifndef H2G_P2P_STAGE_BYTES
+#define H2G_P2P_STAGE_BYTES 4096
+#endif
+constexpr int kP2PStageBytes = H2G_P2P_STAGE_BYTES;       // one stage slot
+constexpr int kP2PSlotsPerWarp = 2;                       // stages in flight per warp
+constexpr int kP2PSlots = kP2PSlotsPerWarp * kP2PWarps;   // slot ring per CTA
+// dynamic smem of the P2P kernel: stage slots + the chunk buffers + the
+// cross-warp reduction + mbarriers
+constexpr size_t kP2PSmem = (size_t)kP2PSlots * kP2PStageBytes +
+                            (size_t)kP2PWarps * 2 * kP2PChunk * (sizeof(double) * 4 + 8) +
+                            (size_t)kP2PWarps * kMaxRows * 8 + (size_t)kP2PSlots * 8 + 16;
 
 // Host-built work lists of the P2P engine (from the Task/Term schedule):
-struct P2PTask {       // 32 bytes
+struct P2PTask {       // 40 bytes
   int64_t y_off;       // arena slot of y[0]
   int32_t m;           // rows (<= kMaxRows)
   int32_t row_rec;     // record of row 0
-  int32_t t_begin;     // stored GEMV terms [t_begin, t_end) of the Term table
+  int32_t t_begin;     // stored GEMV terms [t_begin, t_end) of the Term table (direct loads)
   int32_t t_end;
   int32_t k_begin;     // evaluated chunks [k_begin, k_end) of the chunk table
   int32_t k_end;
+  int32_t s_begin;     // TMA-staged stored columns [s_begin, s_end) of the stage table
+  int32_t s_end;
+};
+
+// STAGED stored data: the stored blocks of a task with contiguous columns
+// (lda == m: stored M2L blocks, L2L, L2P, BLR U, near) are cut into stages of
+// <= kP2PStageBytes, each ONE cp.async.bulk into a per-warp smem slot, issued
+// ahead and consumed between the warp's evaluated chunks -- so HBM streams
+// while the fp64 pipe evaluates (m2l_recompute_share < 1: a share of every
+// target's M2L blocks is read, the rest evaluated).
+struct P2PStage {      // 24 bytes
+  uint64_t src;        // 16-byte aligned global address of the copy
+  int64_t x_off;       // arena slot of x for column 0
+  uint32_t bytes;      // copy bytes (multiple of 16)
+  int16_t ncols;       // columns (of m rows, column-major, contiguous)
+  int16_t shift;       // A(0, 0) at slot + shift doubles
 };
 
 struct P2PChunk {      // 16 bytes: <= 32 columns of one evaluated block
@@ -70,17 +98,35 @@ struct P2PChunk {      // 16 bytes: <= 32 columns of one evaluated block
   int32_t n_self;      // columns | kSelfBit (row and column runs share points)
 };
 
+__device__ __forceinline__ void issue_stage(const P2PStage& st, double* slot, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot done
+  mbar_arrive_expect_tx(bar, st.bytes);
+  bulk_g2s(slot, reinterpret_cast<const void*>(st.src), st.bytes, bar);
+}
+
 template <int KT, int DIM, int L, int J>
 __device__ __forceinline__ void p2p_task(const P2PTask& tk, const Term* __restrict__ terms,
                                          const P2PChunk* __restrict__ chunks,
+                                         const P2PStage* __restrict__ stages,
                                          const double4* __restrict__ recs,
                                          const double* __restrict__ blob, double* arena,
                                          const P2PKernel& kp, double4 (*srec)[kP2PChunk],
-                                         double (*sx)[kP2PChunk], double* red, int lane,
-                                         int warp) {
+                                         double (*sx)[kP2PChunk], double* red, double* slots,
+                                         uint64_t* sbar, uint32_t& sphase, int lane, int warp) {
   constexpr int G = 32 / L;
   const int g = lane / L, rl = lane % L;
   const int m = tk.m;
+  // stages of this warp: s = s_begin + warp + kP2PWarps i, in slot
+  // warp + kP2PWarps (i % kP2PSlotsPerWarp); the first ones go out now
+  const int n_st = tk.s_end - tk.s_begin;
+  if (lane == 0)
+    for (int i = 0; i < kP2PSlotsPerWarp; ++i) {
+      const int si = warp + kP2PWarps * i;
+      if (si < n_st) {
+        const int sl = warp + kP2PWarps * i;
+        issue_stage(stages[tk.s_begin + si], slots + (size_t)sl * (kP2PStageBytes / 8), &sbar[sl]);
+      }
+    }
   const int64_t row0 = tk.row_rec;
   double px[J], py[J], pz[J], acc[J];
 #pragma unroll
@@ -115,6 +161,35 @@ __device__ __forceinline__ void p2p_task(const P2PTask& tk, const Term* __restri
     }
   }
   int buf = 0;
+  int my_si = warp;  // next stage of this warp (index into the task's stages)
+  int my_i = 0;      // its ordinal among the warp's stages (slot = my_i % kP2PSlotsPerWarp)
+  // one staged stored block: columns dealt over the lane groups, rows over
+  // the lanes of a group (the layout of the evaluated chunks)
+  auto consume_stage = [&]() {
+    const int sl = warp + kP2PWarps * (my_i % kP2PSlotsPerWarp);
+    const P2PStage st = stages[tk.s_begin + my_si];
+    mbar_wait(&sbar[sl], (sphase >> sl) & 1u);
+    sphase ^= 1u << sl;
+    const double* A = slots + (size_t)sl * (kP2PStageBytes / 8) + st.shift;
+    const double* x = arena + st.x_off;
+    const int nc = st.ncols;
+#pragma unroll 2
+    for (int c = g; c < nc; c += G) {
+      const double xv = x[c];
+      const double* col = A + c * m;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int r = rl + L * j;
+        if (r < m) acc[j] = fma(col[r], xv, acc[j]);
+      }
+    }
+    __syncwarp();
+    const int nxt = my_si + kP2PWarps * kP2PSlotsPerWarp;
+    if (lane == 0 && nxt < n_st)
+      issue_stage(stages[tk.s_begin + nxt], slots + (size_t)sl * (kP2PStageBytes / 8), &sbar[sl]);
+    my_si += kP2PWarps;
+    ++my_i;
+  };
   while (k < tk.k_end) {
     const int n = cd.n_self & 0xffff;
     const bool self = (cd.n_self & kSelfBit) != 0;
@@ -170,7 +245,9 @@ __device__ __forceinline__ void p2p_task(const P2PTask& tk, const Term* __restri
       }
     }
     buf ^= 1;
+    if (my_si < n_st) consume_stage();  // one staged block between evaluated chunks
   }
+  while (my_si < n_st) consume_stage();
   // ---- stored terms (L2L, L2P, BLR U, stored blocks): columns dealt over
   // (warp, lane group) pairs, direct coalesced loads down each column
   for (int t = tk.t_begin; t < tk.t_end; ++t) {
@@ -222,10 +299,12 @@ constexpr int kP2PRowsPerLane = H2G_P2P_JT;
 template <int KT, int DIM>
 __device__ __forceinline__ void p2p_dispatch(const P2PTask& tk, const Term* __restrict__ terms,
                                              const P2PChunk* __restrict__ chunks,
+                                             const P2PStage* __restrict__ stages,
                                              const double4* __restrict__ recs,
                                              const double* __restrict__ blob, double* arena,
                                              const P2PKernel& kp, double4 (*srec)[kP2PChunk],
-                                             double (*sx)[kP2PChunk], double* red, int lane,
+                                             double (*sx)[kP2PChunk], double* red, double* slots,
+                                             uint64_t* sbar, uint32_t& sphase, int lane,
                                              int warp) {
   const int m = tk.m;
   constexpr int JT = kP2PRowsPerLane;
@@ -233,8 +312,8 @@ __device__ __forceinline__ void p2p_dispatch(const P2PTask& tk, const Term* __re
   while (L < 32 && L * JT < m) L <<= 1;
   const int J = (m + L - 1) / L;
 #define H2G_P2P(Lv, Jv)                                                                     \
-  p2p_task<KT, DIM, Lv, Jv>(tk, terms, chunks, recs, blob, arena, kp, srec, sx, red, lane, \
-                            warp)
+  p2p_task<KT, DIM, Lv, Jv>(tk, terms, chunks, stages, recs, blob, arena, kp, srec, sx, red, \
+                            slots, sbar, sphase, lane, warp)
 #define H2G_P2P_J(Lv)                                                  \
   switch (J) {                                                         \
     case 1: if constexpr (Lv == 4) { H2G_P2P(Lv, 1); } else { __trap(); } break;          \
@@ -266,23 +345,32 @@ __device__ __forceinline__ void p2p_dispatch(const P2PTask& tk, const Term* __re
 template <int KT, int DIM>
 __global__ void __launch_bounds__(kP2PThreads, kP2PCtasPerSm)
 p2p_tasks_kernel(const P2PTask* __restrict__ tasks, int n_tasks, const Term* __restrict__ terms,
-                 const P2PChunk* __restrict__ chunks, const double4* __restrict__ recs,
-                 const double* __restrict__ blob, double* arena, P2PKernel kp, int* ctr) {
-  __shared__ double4 srec[kP2PWarps][2][kP2PChunk];
-  __shared__ double sx[kP2PWarps][2][kP2PChunk];
-  __shared__ double red[kP2PWarps * kMaxRows];
-  __shared__ int s_task;
+                 const P2PChunk* __restrict__ chunks, const P2PStage* __restrict__ stages,
+                 const double4* __restrict__ recs, const double* __restrict__ blob,
+                 double* arena, P2PKernel kp, int* ctr) {
+  extern __shared__ __align__(128) double p2p_smem[];
+  double* slots = p2p_smem;  // kP2PSlots x kP2PStageBytes
+  auto srec = reinterpret_cast<double4 (*)[2][kP2PChunk]>(slots + kP2PSlots * (kP2PStageBytes / 8));
+  auto sx = reinterpret_cast<double (*)[2][kP2PChunk]>(srec + kP2PWarps);
+  double* red = reinterpret_cast<double*>(sx + kP2PWarps);
+  uint64_t* sbar = reinterpret_cast<uint64_t*>(red + kP2PWarps * kMaxRows);
+  int* s_task = reinterpret_cast<int*>(sbar + kP2PSlots);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kP2PSlots; ++i) mbar_init(&sbar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t sphase = 0;  // parity of every slot's barrier (bit per slot; a warp touches its own)
   griddep_launch_dependents();
   griddep_wait();  // x (and the counters' reset) come from earlier phases
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(ctr, 1);
+    if (threadIdx.x == 0) *s_task = atomicAdd(ctr, 1);
     __syncthreads();
-    const int t = s_task;
+    const int t = *s_task;
     if (t >= n_tasks) break;
     const P2PTask tk = tasks[t];
-    p2p_dispatch<KT, DIM>(tk, terms, chunks, recs, blob, arena, kp, srec[warp], sx[warp], red,
-                          lane, warp);
+    p2p_dispatch<KT, DIM>(tk, terms, chunks, stages, recs, blob, arena, kp, srec[warp], sx[warp],
+                          red, slots, sbar, sphase, lane, warp);
     __syncthreads();  // red / s_task reuse
   }
   if (threadIdx.x == 0) {

@@ -217,6 +217,7 @@ struct h2g_plan {
   P2PTask* d_p2p_tasks = nullptr;
   Term* d_p2p_terms = nullptr;     // stored terms of the P2P tasks
   P2PChunk* d_p2p_chunks = nullptr;
+  P2PStage* d_p2p_stages = nullptr;
   int* d_ctr = nullptr;        // 2 task counters per phase
   P2PKernel kp{};
   int kernel_type = -1;
@@ -537,9 +538,12 @@ inline int64_t stream_end_of(const Phase& ph) {
 
 // P2P work lists: per task its stored terms (own table) and its evaluated
 // terms cut into <= kP2PChunk-column chunks.
+// (stored blocks with contiguous columns -- lda == m, in the blob -- become
+// TMA stages of <= kP2PStageBytes, staged through the warps' smem slots)
 void build_p2p_lists(const HostSchedule& s, std::vector<Phase>& phases,
                      std::vector<P2PTask>& pt, std::vector<Term>& pterms,
-                     std::vector<P2PChunk>& pch) {
+                     std::vector<P2PChunk>& pch, std::vector<P2PStage>& pst,
+                     const double* d_blob) {
   for (Phase& ph : phases) {
     ph.p2p_off = (int64_t)pt.size();
     for (int64_t i = stream_end_of(ph); i < ph.task_end; ++i) {
@@ -550,8 +554,26 @@ void build_p2p_lists(const HostSchedule& s, std::vector<Phase>& phases,
       q.row_rec = t.pad;
       q.t_begin = (int32_t)pterms.size();
       q.k_begin = (int32_t)pch.size();
+      q.s_begin = (int32_t)pst.size();
       for (int32_t k = t.t_begin; k < t.t_end; ++k) {
         const Term& tm = s.terms[k];
+        if (tm.a_space == 0 && tm.lda == t.m && tm.ncols > 0 && d_blob) {
+          const int64_t cc = std::max<int64_t>(1, (kP2PStageBytes - 16) / (8 * (int64_t)t.m));
+          for (int64_t c0 = 0; c0 < tm.ncols; c0 += cc) {
+            const int64_t nc = std::min<int64_t>(cc, tm.ncols - c0);
+            const uint64_t src = reinterpret_cast<uint64_t>(d_blob + tm.a_off + c0 * t.m);
+            const uint64_t a = src & ~uint64_t(15);
+            const uint64_t e = (src + 8ull * (uint64_t)(t.m * nc) + 15) & ~uint64_t(15);
+            P2PStage st{};
+            st.src = a;
+            st.x_off = tm.x_off + c0;
+            st.bytes = (uint32_t)(e - a);
+            st.ncols = (int16_t)nc;
+            st.shift = (int16_t)((src - a) / 8);
+            pst.push_back(st);
+          }
+          continue;
+        }
         if (tm.a_space != kRecompute) {
           pterms.push_back(tm);
           continue;
@@ -566,6 +588,7 @@ void build_p2p_lists(const HostSchedule& s, std::vector<Phase>& phases,
       }
       q.t_end = (int32_t)pterms.size();
       q.k_end = (int32_t)pch.size();
+      q.s_end = (int32_t)pst.size();
       pt.push_back(q);
     }
   }
@@ -1308,9 +1331,10 @@ int launch_p2p(h2g_plan* p, const Phase& ph, int phase_idx, cudaStream_t s, bool
   int* ctr = p->d_ctr + 2 * phase_idx;
   const int kt = p->kernel_type, d3 = p->dim >= 3;
 #define H2G_LAUNCH_P2P(KT, DIM)                                                              \
-  CUDA_TRY(launch_k(p->pdl && pdl, p2p_tasks_kernel<KT, DIM>, grid, kP2PThreads, 0, s, tk, (int)n,  \
-                    (const Term*)p->d_p2p_terms, (const P2PChunk*)p->d_p2p_chunks,             \
-                    (const double4*)p->d_recs4, (const double*)p->d_blob, p->d_arena, p->kp, ctr))
+  CUDA_TRY(launch_k(p->pdl && pdl, p2p_tasks_kernel<KT, DIM>, grid, kP2PThreads, kP2PSmem, s, tk, \
+                    (int)n, (const Term*)p->d_p2p_terms, (const P2PChunk*)p->d_p2p_chunks,     \
+                    (const P2PStage*)p->d_p2p_stages, (const double4*)p->d_recs4,             \
+                    (const double*)p->d_blob, p->d_arena, p->kp, ctr))
   if (kt == 0) {
     if (d3) H2G_LAUNCH_P2P(0, 3); else H2G_LAUNCH_P2P(0, 2);
   } else if (kt == 1) {
@@ -1445,6 +1469,7 @@ void free_plan(h2g_plan* p) {
   cudaFree(p->d_p2p_tasks);
   cudaFree(p->d_p2p_terms);
   cudaFree(p->d_p2p_chunks);
+  cudaFree(p->d_p2p_stages);
   cudaFree(p->d_ctr);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
@@ -1710,15 +1735,19 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
       std::vector<P2PTask> pt;
       std::vector<Term> pterms;
       std::vector<P2PChunk> pch;
-      build_p2p_lists(s, p->phases, pt, pterms, pch);
-      if ((int64_t)pch.size() >= (1LL << 31)) return fail(H2G_ERR_BAD_EXPORT, "too many chunks");
+      std::vector<P2PStage> pst;
+      build_p2p_lists(s, p->phases, pt, pterms, pch, pst, p->d_blob);
+      if ((int64_t)pch.size() >= (1LL << 31) || (int64_t)pst.size() >= (1LL << 31))
+        return fail(H2G_ERR_BAD_EXPORT, "too many chunks");
+      if ((r = upload((void**)&p->d_p2p_stages, pst.data(), sizeof(P2PStage) * pst.size())))
+        return r;
       if ((r = upload((void**)&p->d_p2p_tasks, pt.data(), sizeof(P2PTask) * pt.size()))) return r;
       if ((r = upload((void**)&p->d_p2p_terms, pterms.data(), sizeof(Term) * pterms.size())))
         return r;
       if ((r = upload((void**)&p->d_p2p_chunks, pch.data(), sizeof(P2PChunk) * pch.size())))
         return r;
       p->workspace_bytes += sizeof(P2PTask) * pt.size() + sizeof(Term) * pterms.size() +
-                            sizeof(P2PChunk) * pch.size();
+                            sizeof(P2PChunk) * pch.size() + sizeof(P2PStage) * pst.size();
       CUDA_TRY(cudaMalloc((void**)&p->d_ctr, sizeof(int) * 2 * std::max<size_t>(1, p->phases.size())));
       CUDA_TRY(cudaMemset(p->d_ctr, 0, sizeof(int) * 2 * std::max<size_t>(1, p->phases.size())));
     }
@@ -1731,7 +1760,9 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     // P2P kernels: maximum shared-memory carve-out (L1 is not what they need)
 #define H2G_P2P_CARVEOUT(KT, DIM)                                                       \
   CUDA_TRY(cudaFuncSetAttribute(p2p_tasks_kernel<KT, DIM>,                              \
-                                cudaFuncAttributePreferredSharedMemoryCarveout, 100))
+                                cudaFuncAttributePreferredSharedMemoryCarveout, 100));  \
+  CUDA_TRY(cudaFuncSetAttribute(p2p_tasks_kernel<KT, DIM>,                              \
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2PSmem))
     H2G_P2P_CARVEOUT(0, 2);
     H2G_P2P_CARVEOUT(0, 3);
     H2G_P2P_CARVEOUT(1, 2);

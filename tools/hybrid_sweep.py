@@ -2,9 +2,12 @@
 streamed on the streaming engine while the P2P engine evaluates the rest,
 concurrently (h2g_plan.cu, Phase.hybrid; env H2G_M2L_STREAM_SHARE).
 
-    python tools/hybrid_sweep.py [cfg3|N,d,kernel,eps] [shares...]
+    python tools/hybrid_sweep.py [cfg3|N,d,kernel,eps] [modes...]
 
-Prints one JSON line per share: ms per matvec (CUDA events, 20 matvecs after
+modes: "hF" = hybrid phases with share F of the M2L entries streamed on the
+streaming engine beside the P2P engine; "sF" = m2l_recompute_share F (share
+EVALUATED; the rest of every target's M2L blocks TMA-staged inside the P2P
+tasks); "s1" = all evaluated.  Prints one JSON line per mode: ms per matvec (CUDA events, 20 matvecs after
 5 warm-ups), per-phase us, error vs the all-streamed result.  Diagnostics
 only; bench.py is the measured contract.
 """
@@ -29,7 +32,7 @@ def main():
     else:
         a = spec.split(",")
         N, d, kernel, eps = int(a[0]), int(a[1]), a[2], float(a[3])
-    shares = [float(x) for x in sys.argv[2:]] or [0.0, 0.2, 0.3, 0.4, 0.5]
+    modes = sys.argv[2:] or ["s1", "s0.7", "s0.6", "s0.5"]
     t0 = time.time()
     op = build_variant("h2star-bt", uniform_points(N, d, 42), kernel, 64, eps)
     print(json.dumps({"build_s": time.time() - t0, "N": N, "mem_GB": op.mem_scalars * 8e-9}),
@@ -40,9 +43,15 @@ def main():
     with GpuHierRep(op) as rep:
         base = rep.matvec(q)
     stream = torch.cuda.Stream()
-    for sh in shares:
-        os.environ["H2G_M2L_STREAM_SHARE"] = str(sh)
-        with GpuHierRep(op, recompute="m2l") as rep:
+    for mode in modes:
+        sh = float(mode[1:])
+        if mode[0] == "h":
+            os.environ["H2G_M2L_STREAM_SHARE"] = str(sh)
+            kw = {}
+        else:
+            os.environ.pop("H2G_M2L_STREAM_SHARE", None)
+            kw = {"m2l_share": sh}
+        with GpuHierRep(op, recompute="m2l", **kw) as rep:
             L, plan = rep._L, rep._plan
             for _ in range(5):
                 L.h2g_matvec(plan, qd.data_ptr(), out.data_ptr(), N, 1, 1, stream.cuda_stream)
@@ -57,7 +66,7 @@ def main():
             phi = out.cpu().numpy().copy()
             prof = rep.profile_phases(qd, out, iters=5)
             err = float(np.linalg.norm(phi - base) / np.linalg.norm(base))
-            print(json.dumps({"share": sh, "ms": ms, "matvec_per_s": 1e3 / ms, "err_vs_streamed": err,
+            print(json.dumps({"mode": mode, "ms": ms, "matvec_per_s": 1e3 / ms, "err_vs_streamed": err,
                               "launches": rep.launches_per_matvec(),
                               "phases_us": {p["phase"]: round(p["ms"] * 1e3, 1) for p in prof}}),
                   flush=True)
