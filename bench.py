@@ -206,6 +206,13 @@ def cpu_port_time(op, q, budget_s=15.0, max_steps=20):
     return time_sampled_matvec(op, q, steps=max_steps, warmup=0, budget_s=budget_s)
 
 
+# Share of the STORED M2L entries the P2P engine evaluates when it evaluates
+# M2L; the rest of every target's blocks stream (TMA-staged) inside the same
+# tasks, so HBM and the fp64 pipe work at once (tools/hybrid_sweep.py, cfg 3:
+# 1.0 -> 11.69 ms, 0.8 -> 11.14, 0.7 -> 10.92, 0.6 -> 11.16, 0.5 -> 11.58).
+M2L_EVAL_SHARE = 0.7
+
+
 def recompute_for(cfg, arg, op=None):
     """Which raw kernel blocks the device evaluates instead of streaming
     (csrc/h2g_p2p.cuh).  "auto": whichever the measurements say is faster
@@ -320,7 +327,7 @@ def _time_steps(step, args, torch, dev, stream, world):
 
 def bench_variant(op, args, torch, dev, rank, world, recompute="", e2e=True):
     from paper_2309_14085_b200.gpu_rep import GpuHierRep
-    rep = GpuHierRep(op, device=dev, recompute=recompute)
+    rep = GpuHierRep(op, device=dev, recompute=recompute, m2l_share=args.m2l_share)
     N = op.N
     q = np.random.default_rng(43).standard_normal(N)
     qd = torch.from_numpy(q).to(f"cuda:{dev}")
@@ -364,7 +371,8 @@ def bench_variant(op, args, torch, dev, rank, world, recompute="", e2e=True):
 def bench_variant_sharded(op, args, torch, dev, rank, world, recompute=""):
     """Strong scaling: the operator split over `world` GPUs, one all-gather."""
     from paper_2309_14085_b200.sharded import ShardedGpuHierRep
-    rep = ShardedGpuHierRep(op, rank, world, device=dev, recompute=recompute)
+    rep = ShardedGpuHierRep(op, rank, world, device=dev, recompute=recompute,
+                            m2l_share=args.m2l_share)
     N = op.N
     q = np.random.default_rng(43).standard_normal(N)
     qd = torch.from_numpy(q).to(f"cuda:{dev}")
@@ -444,6 +452,9 @@ def main():
     ap.add_argument("--streamed-variant", type=int, default=1,
                     help="also time the all-streamed plan (pure HBM fraction) when the headline "
                          "evaluates blocks")
+    ap.add_argument("--m2l-share", type=float, default=M2L_EVAL_SHARE,
+                    help="share of the stored M2L entries evaluated when M2L is evaluated "
+                         "(the rest streams inside the same P2P tasks); 1 = all evaluated")
     ap.add_argument("--nrhs", type=int, default=16,
                     help="also time the batched-RHS engine with this many right-hand sides")
     args = ap.parse_args()
@@ -535,7 +546,9 @@ def main():
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (uniform_points seed 42, q ~ N(0,1) seed 43)",
         "config": config_dict(cfg, head, N, op.kappa, S, world),
-        "evaluated_blocks": rc or "none", "build_s": round(R["build_s"], 2),
+        "evaluated_blocks": rc or "none",
+        "m2l_eval_share": args.m2l_share if "m2l" in (rc or "") and cfg.get("store") != "" else None,
+        "build_s": round(R["build_s"], 2),
         "achieved_GBps": alg_bytes / (R["ms"] * 1e-3) / 1e9,
         "roofline": roof,
         "e2e": {"value": 1.0 / R["e2e_s"], "unit": "matvec/s",

@@ -22,6 +22,7 @@
 // atomic-free and bitwise repeatable.  The middle phases are captured once
 // into a CUDA graph.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <map>
@@ -46,6 +47,13 @@ int fail(int code, const std::string& msg) {
   g_detail = msg;
   return code;
 }
+
+// Scoped NVTX range around every ABI entry (host-side work and launches;
+// kernels show up under it in a timeline; no-ops without a tool attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 #define CUDA_TRY(expr)                                                               \
   do {                                                                               \
@@ -543,7 +551,7 @@ inline int64_t stream_end_of(const Phase& ph) {
 void build_p2p_lists(const HostSchedule& s, std::vector<Phase>& phases,
                      std::vector<P2PTask>& pt, std::vector<Term>& pterms,
                      std::vector<P2PChunk>& pch, std::vector<P2PStage>& pst,
-                     const double* d_blob) {
+                     const double* d_blob, bool stage) {
   for (Phase& ph : phases) {
     ph.p2p_off = (int64_t)pt.size();
     for (int64_t i = stream_end_of(ph); i < ph.task_end; ++i) {
@@ -557,7 +565,7 @@ void build_p2p_lists(const HostSchedule& s, std::vector<Phase>& phases,
       q.s_begin = (int32_t)pst.size();
       for (int32_t k = t.t_begin; k < t.t_end; ++k) {
         const Term& tm = s.terms[k];
-        if (tm.a_space == 0 && tm.lda == t.m && tm.ncols > 0 && d_blob) {
+        if (stage && tm.a_space == 0 && tm.lda == t.m && tm.ncols > 0 && d_blob) {
           const int64_t cc = std::max<int64_t>(1, (kP2PStageBytes - 16) / (8 * (int64_t)t.m));
           for (int64_t c0 = 0; c0 < tm.ncols; c0 += cc) {
             const int64_t nc = std::min<int64_t>(cc, tm.ncols - c0);
@@ -1736,7 +1744,12 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
       std::vector<Term> pterms;
       std::vector<P2PChunk> pch;
       std::vector<P2PStage> pst;
-      build_p2p_lists(s, p->phases, pt, pterms, pch, pst, p->d_blob);
+      // stage stored blocks through TMA when a share of the M2L blocks streams
+      // inside the P2P tasks (measured: staging only the small L2L / L2P
+      // terms of all-evaluated tasks costs ~3 %; direct loads there)
+      const bool stage = d->m2l_recompute_share > 0.0 && d->m2l_recompute_share < 1.0 &&
+                         (d->recompute & H2G_RECOMPUTE_M2L);
+      build_p2p_lists(s, p->phases, pt, pterms, pch, pst, p->d_blob, stage);
       if ((int64_t)pch.size() >= (1LL << 31) || (int64_t)pst.size() >= (1LL << 31))
         return fail(H2G_ERR_BAD_EXPORT, "too many chunks");
       if ((r = upload((void**)&p->d_p2p_stages, pst.data(), sizeof(P2PStage) * pst.size())))
@@ -2005,6 +2018,7 @@ const char* h2g_error_string(int code) {
 const char* h2g_last_error_detail(void) { return g_detail.c_str(); }
 
 int h2g_plan_create(const h2g_export_desc* desc, int device, h2g_plan** out) {
+  NvtxRange nvtx_range_("h2g_plan_create");
   if (!out) return fail(H2G_ERR_INVALID_ARG, "null out");
   *out = nullptr;
   return create_impl(desc, device, out);
@@ -2012,6 +2026,7 @@ int h2g_plan_create(const h2g_export_desc* desc, int device, h2g_plan** out) {
 
 int h2g_plan_create_sharded(const h2g_export_desc* desc, int device, int rank, int nranks,
                             h2g_plan** out) {
+  NvtxRange nvtx_range_("h2g_plan_create_sharded");
   if (!out) return fail(H2G_ERR_INVALID_ARG, "null out");
   *out = nullptr;
   return create_impl(desc, device, out, rank, nranks);
@@ -2033,6 +2048,7 @@ int h2g_shard_get_info(const h2g_plan* p, h2g_shard_info* o) {
 }
 
 int h2g_matvec_begin(h2g_plan* p, const double* q_dev, int64_t n, void* stream) {
+  NvtxRange nvtx_range_("h2g_matvec_begin");
   if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
   if (n != p->N) return fail(H2G_ERR_LENGTH_MISMATCH, "vector length mismatch");
   if (!q_dev) return fail(H2G_ERR_INVALID_ARG, "null vector");
@@ -2051,6 +2067,7 @@ int h2g_matvec_begin(h2g_plan* p, const double* q_dev, int64_t n, void* stream) 
 }
 
 int h2g_shard_pack(h2g_plan* p, double* send_dev, void* stream) {
+  NvtxRange nvtx_range_("h2g_shard_pack");
   if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
   if (p->n_pack == 0) return H2G_OK;
   if (!send_dev) return fail(H2G_ERR_INVALID_ARG, "null buffer");
@@ -2064,6 +2081,7 @@ int h2g_shard_pack(h2g_plan* p, double* send_dev, void* stream) {
 }
 
 int h2g_shard_unpack(h2g_plan* p, const double* recv_dev, void* stream) {
+  NvtxRange nvtx_range_("h2g_shard_unpack");
   if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
   if (p->n_unpack == 0) return H2G_OK;
   if (!recv_dev) return fail(H2G_ERR_INVALID_ARG, "null buffer");
@@ -2077,6 +2095,7 @@ int h2g_shard_unpack(h2g_plan* p, const double* recv_dev, void* stream) {
 }
 
 int h2g_matvec_end(h2g_plan* p, double* phi_dev, int64_t n, void* stream) {
+  NvtxRange nvtx_range_("h2g_matvec_end");
   if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
   if (n != p->N) return fail(H2G_ERR_LENGTH_MISMATCH, "vector length mismatch");
   if (!phi_dev) return fail(H2G_ERR_INVALID_ARG, "null vector");
@@ -2095,6 +2114,7 @@ int h2g_matvec_end(h2g_plan* p, double* phi_dev, int64_t n, void* stream) {
 }
 
 int h2g_shard_load_q(h2g_plan* p, const double* q_own_dev, void* stream) {
+  NvtxRange nvtx_range_("h2g_shard_load_q");
   if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
   const int64_t rows = p->row_end - p->row_begin;
   if (rows > 0 && !q_own_dev) return fail(H2G_ERR_INVALID_ARG, "null vector");
@@ -2109,6 +2129,7 @@ int h2g_shard_load_q(h2g_plan* p, const double* q_own_dev, void* stream) {
 }
 
 int h2g_halo_pack(h2g_plan* p, double* send_dev, void* stream) {
+  NvtxRange nvtx_range_("h2g_halo_pack");
   if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
   if (p->n_hpack == 0) return H2G_OK;
   if (!send_dev) return fail(H2G_ERR_INVALID_ARG, "null buffer");
@@ -2122,6 +2143,7 @@ int h2g_halo_pack(h2g_plan* p, double* send_dev, void* stream) {
 }
 
 int h2g_halo_unpack(h2g_plan* p, const double* recv_dev, void* stream) {
+  NvtxRange nvtx_range_("h2g_halo_unpack");
   if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
   if (p->n_hunpack == 0) return H2G_OK;
   if (!recv_dev) return fail(H2G_ERR_INVALID_ARG, "null buffer");
@@ -2135,6 +2157,7 @@ int h2g_halo_unpack(h2g_plan* p, const double* recv_dev, void* stream) {
 }
 
 int h2g_shard_part0(h2g_plan* p, void* stream) {
+  NvtxRange nvtx_range_("h2g_shard_part0");
   if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
   if (p->shard.nranks == 1) return fail(H2G_ERR_INVALID_ARG, "not a sharded plan");
   CUDA_TRY(cudaSetDevice(p->device));
@@ -2146,6 +2169,7 @@ int h2g_shard_part0(h2g_plan* p, void* stream) {
 }
 
 int h2g_shard_store_phi(h2g_plan* p, double* phi_own_dev, void* stream) {
+  NvtxRange nvtx_range_("h2g_shard_store_phi");
   if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
   const int64_t rows = p->row_end - p->row_begin;
   if (rows > 0 && !phi_own_dev) return fail(H2G_ERR_INVALID_ARG, "null vector");
@@ -2202,11 +2226,13 @@ int h2g_launches_per_matvec(const h2g_plan* p, int64_t nrhs) {
 
 int h2g_matvec(h2g_plan* plan, const double* q_dev, double* phi_dev, int64_t n, int64_t nrhs,
                int64_t ld, void* stream) {
+  NvtxRange nvtx_range_("h2g_matvec");
   return matvec_impl(plan, q_dev, phi_dev, n, nrhs, ld, (cudaStream_t)stream);
 }
 
 int h2g_matvec_host(h2g_plan* p, const double* q_host, double* phi_host, int64_t n, int64_t nrhs,
                     int64_t ld) {
+  NvtxRange nvtx_range_("h2g_matvec_host");
   int rc = check_vec_args(p, n, nrhs, ld);
   if (rc) return rc;
   if (!q_host || !phi_host) return fail(H2G_ERR_INVALID_ARG, "null vector");
@@ -2449,6 +2475,7 @@ int h2g_schedule_info(const h2g_export_desc* desc, int n_sm, char* buf, int64_t 
 // the arena's current contents (timing does not depend on the values).
 int h2g_profile_phases_batched(h2g_plan* p, int kb, int iters, double* ms, int64_t* bytes,
                                const char** names, int cap, int* n_out) {
+  NvtxRange nvtx_range_("h2g_profile_phases_batched");
   if (!p || iters < 1 || (kb != 8 && kb != 16)) return fail(H2G_ERR_INVALID_ARG, "bad argument");
   if (p->engine != 1 || p->has_p2p || p->shard.nranks > 1)
     return fail(H2G_ERR_INVALID_ARG, "batched engine not available for this plan");
@@ -2507,6 +2534,7 @@ int h2g_profile_phases_batched(h2g_plan* p, int kb, int iters, double* ms, int64
 
 int h2g_profile_phases(h2g_plan* p, const double* q_dev, double* phi_dev, int iters, double* ms,
                        int64_t* bytes, const char** names, int cap, int* n_out) {
+  NvtxRange nvtx_range_("h2g_profile_phases");
   if (!p || !q_dev || !phi_dev || iters < 1) return fail(H2G_ERR_INVALID_ARG, "bad argument");
   CUDA_TRY(cudaSetDevice(p->device));
   const int nph = (int)p->phases.size() + 2;  // + gather + scatter

@@ -40,10 +40,10 @@ class ShardedGpuHierRep:
     config 5's operating mode, whose stored blocks would not fit."""
 
     def __init__(self, op: PackedOperator, rank: int, nranks: int, device: int = 0,
-                 group=None, lib=None, recompute: str = ""):
+                 group=None, lib=None, recompute: str = "", m2l_share: float = 1.0):
         L = lib or _lib.load()
         op.validate()
-        desc, keep = _desc_from_packed(op, recompute)
+        desc, keep = _desc_from_packed(op, recompute, m2l_share)
         plan = C.c_void_p()
         _lib.check(L.h2g_plan_create_sharded(C.byref(desc), int(device), int(rank), int(nranks),
                                              C.byref(plan)), "h2g_plan_create_sharded", L=L)
