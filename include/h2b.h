@@ -77,6 +77,46 @@ void h2b_free(h2b_result* r);
 const char* h2b_last_error(void);
 int h2b_abi_version(void);
 
+/* Materialise the raw kernel blocks of a packed export (the blocks a build
+ * with skip_blocks left out): every M2L block (X, Y) with m2l_off >= 0 is
+ * K[t_i(X), s_o(Y)] (engine.py:176-179, r_in(X) x r_out(Y), column-major)
+ * and every near block with near_off >= 0 is K[t^X, t^Y] (engine.py:309-318,
+ * n_X x n_Y); rows / columns are tree positions into points_tree, entries
+ * follow Kernel.block (kernels.py:36-57) exactly as h2b_build fills them
+ * (bitwise).  Parallel over target clusters (OpenMP). */
+typedef struct h2b_fill_channel {
+  const int32_t* r_in;          /* [n_clusters] */
+  const int32_t* r_out;         /* [n_clusters] */
+  const int64_t* m2l_rowptr;    /* [n_clusters + 1] */
+  const int32_t* m2l_src;       /* [nnz] */
+  const int64_t* m2l_off;       /* [nnz]: blob offset to fill, -1 = skip */
+  const int64_t* piv_in_ptr;    /* [n_clusters + 1] t_i as tree positions */
+  const int64_t* piv_in;
+  const int64_t* piv_out_ptr;   /* [n_clusters + 1] s_o as tree positions */
+  const int64_t* piv_out;
+} h2b_fill_channel;
+
+typedef struct h2b_fill_desc {
+  int32_t dim;
+  int32_t kernel;               /* H2B_KERNEL_* */
+  int32_t has_diag;
+  int32_t n_channels;
+  int64_t n_points;
+  int64_t n_clusters;
+  const double* points_tree;    /* n_points x dim, tree order */
+  double zero_value, diag, shift, sigma;
+  const int64_t* cl_start;      /* [n_clusters] */
+  const int64_t* cl_end;
+  const int64_t* near_rowptr;   /* [n_clusters + 1] */
+  const int32_t* near_src;
+  const int64_t* near_off;      /* blob offset to fill, -1 = skip */
+  h2b_fill_channel channels[2];
+  int32_t n_threads;            /* 0 = OpenMP default */
+  int32_t pad;
+} h2b_fill_desc;
+
+int h2b_fill_kernel_blocks(const h2b_fill_desc* desc, double* blob, int64_t blob_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,8 +42,27 @@ class H2bParams(C.Structure):
                 ("skip_blocks", C.c_int32)]
 
 
+class H2bFillChannel(C.Structure):
+    _fields_ = [("r_in", C.POINTER(C.c_int32)), ("r_out", C.POINTER(C.c_int32)),
+                ("m2l_rowptr", C.POINTER(C.c_int64)), ("m2l_src", C.POINTER(C.c_int32)),
+                ("m2l_off", C.POINTER(C.c_int64)), ("piv_in_ptr", C.POINTER(C.c_int64)),
+                ("piv_in", C.POINTER(C.c_int64)), ("piv_out_ptr", C.POINTER(C.c_int64)),
+                ("piv_out", C.POINTER(C.c_int64))]
+
+
+class H2bFillDesc(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("kernel", C.c_int32), ("has_diag", C.c_int32),
+                ("n_channels", C.c_int32), ("n_points", C.c_int64), ("n_clusters", C.c_int64),
+                ("points_tree", C.POINTER(C.c_double)), ("zero_value", C.c_double),
+                ("diag", C.c_double), ("shift", C.c_double), ("sigma", C.c_double),
+                ("cl_start", C.POINTER(C.c_int64)), ("cl_end", C.POINTER(C.c_int64)),
+                ("near_rowptr", C.POINTER(C.c_int64)), ("near_src", C.POINTER(C.c_int32)),
+                ("near_off", C.POINTER(C.c_int64)), ("channels", H2bFillChannel * 2),
+                ("n_threads", C.c_int32), ("pad", C.c_int32)]
+
+
 H2B_SYMBOLS = ("h2b_build", "h2b_get_array", "h2b_get_scalar", "h2b_get_timing", "h2b_free",
-               "h2b_last_error", "h2b_abi_version")
+               "h2b_last_error", "h2b_abi_version", "h2b_fill_kernel_blocks")
 _LIB = None
 
 
@@ -64,6 +83,7 @@ def load():
     L.h2b_get_timing.argtypes = [C.c_void_p, C.c_char_p]
     L.h2b_get_timing.restype = C.c_double
     L.h2b_free.argtypes = [C.c_void_p]
+    L.h2b_fill_kernel_blocks.argtypes = [C.POINTER(H2bFillDesc), C.POINTER(C.c_double), C.c_int64]
     L.h2b_last_error.restype = C.c_char_p
     if L.h2b_abi_version() != 1:
         raise RuntimeError("libh2b.so ABI mismatch; rebuild")
@@ -181,6 +201,90 @@ def build_variant(variant: str, points, kernel: str = "log2d", n_max: int = 64,
         op.meta["_keepalive"] = R  # blob is a view into the native result
     op.validate()
     return op
+
+
+def materialize_blocks(op: PackedOperator, near: bool = True, m2l: bool = True,
+                       n_threads: int = 0) -> PackedOperator:
+    """A copy of ``op`` whose NOT-stored raw kernel blocks (offset -1: an
+    export built with store="" or a compact fixture) are evaluated into the
+    blob by the native builder (h2b_fill_kernel_blocks, include/h2b.h):
+    M2L = K[t_i(X), s_o(Y)] (engine.py:176-179) in target-major order (each
+    target's row contiguous, as a stored build lays it out), near = K[t^X,
+    t^Y] (engine.py:309-318) leaf by leaf.  Bitwise the blocks a stored
+    build holds; seconds instead of the NCA pivot search."""
+    import copy
+    L = load()
+    kname = op.kernel.get("name")
+    if kname not in KERNELS or op.points_tree is None:
+        raise ValueError("materialize_blocks needs points_tree and a known kernel")
+    out = copy.copy(op)
+    n = len(op.blob)
+    keep = []
+
+    def arr(a, dt):
+        a = np.ascontiguousarray(a, dtype=dt)
+        keep.append(a)
+        return a
+
+    def p64(a):
+        return arr(a, np.int64).ctypes.data_as(C.POINTER(C.c_int64))
+
+    def p32(a):
+        return arr(a, np.int32).ctypes.data_as(C.POINTER(C.c_int32))
+
+    f = H2bFillDesc()
+    f.dim, f.kernel, f.n_channels = op.dim, KERNELS[kname], len(op.channels)
+    f.has_diag = op.kernel.get("diag") is not None
+    f.n_points, f.n_clusters = op.N, op.n_clusters
+    f.points_tree = arr(op.points_tree, np.float64).ctypes.data_as(C.POINTER(C.c_double))
+    f.zero_value = float(op.kernel.get("zero_value") or 0.0)
+    f.diag = float(op.kernel.get("diag") or 0.0)
+    f.shift = float(op.kernel.get("shift") or 0.0)
+    f.sigma = float(op.kernel.get("sigma") or 0.1)
+    f.cl_start, f.cl_end = p64(op.cl_start), p64(op.cl_end)
+    f.n_threads = int(n_threads)
+    out.channels = []
+    for i, ch in enumerate(op.channels):
+        ch2 = copy.copy(ch)
+        offs = np.full_like(ch.m2l_off, -1)
+        if m2l:
+            todo = np.flatnonzero(ch.m2l_off < 0)
+            if len(todo):
+                x = np.repeat(np.arange(op.n_clusters), np.diff(ch.m2l_rowptr))[todo]
+                sz = ch.r_in[x].astype(np.int64) * ch.r_out[ch.m2l_src[todo]].astype(np.int64)
+                offs[todo] = n + np.concatenate([[0], np.cumsum(sz)[:-1]])
+                n += int(sz.sum())
+        ch2.m2l_off = np.where(ch.m2l_off < 0, offs, ch.m2l_off)
+        out.channels.append(ch2)
+        c = f.channels[i]
+        c.r_in, c.r_out = p32(ch.r_in), p32(ch.r_out)
+        c.m2l_rowptr, c.m2l_src, c.m2l_off = p64(ch.m2l_rowptr), p32(ch.m2l_src), p64(offs)
+        c.piv_in_ptr, c.piv_in = p64(ch.piv_in_ptr), p64(ch.piv_in)
+        c.piv_out_ptr, c.piv_out = p64(ch.piv_out_ptr), p64(ch.piv_out)
+    noffs = np.full_like(op.near_off, -1)
+    if near:
+        todo = np.flatnonzero(op.near_off < 0)
+        if len(todo):
+            x = np.repeat(np.arange(op.n_clusters), np.diff(op.near_rowptr))[todo]
+            y = op.near_src[todo]
+            sz = (op.cl_end[x] - op.cl_start[x]) * (op.cl_end[y] - op.cl_start[y])
+            noffs[todo] = n + np.concatenate([[0], np.cumsum(sz)[:-1]])
+            n += int(sz.sum())
+    out.near_off = np.where(op.near_off < 0, noffs, op.near_off)
+    f.near_rowptr, f.near_src, f.near_off = p64(op.near_rowptr), p32(op.near_src), p64(noffs)
+    blob = np.empty(n + 4, dtype=np.float64)
+    blob[:len(op.blob)] = op.blob
+    blob[n:] = 0.0
+    rc = L.h2b_fill_kernel_blocks(C.byref(f), blob.ctypes.data_as(C.POINTER(C.c_double)),
+                                  len(blob))
+    if rc:
+        raise RuntimeError(f"h2b_fill_kernel_blocks failed ({rc}): {L.h2b_last_error().decode()}")
+    del keep
+    out.blob = blob
+    out.meta = dict(op.meta)
+    out.meta.pop("_keepalive", None)
+    out.validate()
+    return out
 
 
 def uniform_points(N: int, d: int, seed: int = 42) -> np.ndarray:

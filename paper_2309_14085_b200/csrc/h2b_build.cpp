@@ -1174,6 +1174,72 @@ int build_impl(const h2b_params* P, h2b_result** out) {
 extern "C" {
 
 int h2b_abi_version(void) { return H2B_ABI_VERSION; }
+
+int h2b_fill_kernel_blocks(const h2b_fill_desc* f, double* blob, int64_t blob_len) {
+  if (!f || !blob || !f->points_tree || f->dim < 1 || f->dim > 3 || f->n_channels < 0 ||
+      f->n_channels > 2 || !f->cl_start || !f->cl_end || !f->near_rowptr) {
+    g_err = "h2b_fill_kernel_blocks: bad descriptor";
+    return H2B_ERR_INVALID_ARG;
+  }
+  Kernel K;  // Kernel::entry on tree positions == on original indices (same points)
+  K.type = f->kernel;
+  K.d = f->dim;
+  K.pts = f->points_tree;
+  K.zero_value = f->zero_value;
+  K.diag = f->diag;
+  K.shift = f->shift;
+  K.sigma = f->sigma;
+  K.has_diag = f->has_diag != 0;
+  if (f->n_threads > 0) omp_set_num_threads(f->n_threads);
+  const int64_t nc = f->n_clusters;
+  std::string err;
+  for (int ch = 0; ch < f->n_channels; ++ch) {
+    const h2b_fill_channel& c = f->channels[ch];
+    if (!c.r_in || !c.r_out || !c.m2l_rowptr || (c.m2l_rowptr[nc] > 0 && (!c.piv_in || !c.piv_out))) {
+      g_err = "h2b_fill_kernel_blocks: channel arrays missing";
+      return H2B_ERR_INVALID_ARG;
+    }
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t x = 0; x < nc; ++x) {
+      const int64_t ri = c.r_in[x];
+      for (int64_t k = c.m2l_rowptr[x]; k < c.m2l_rowptr[x + 1]; ++k) {
+        if (c.m2l_off[k] < 0) continue;
+        const int64_t y = c.m2l_src[k];
+        const int64_t ro = c.r_out[y];
+        if (c.m2l_off[k] + ri * ro > blob_len) {
+#pragma omp critical
+          err = "m2l block out of blob";
+          continue;
+        }
+        K.block_cm(c.piv_in + c.piv_in_ptr[x], ri, c.piv_out + c.piv_out_ptr[y], ro,
+                   blob + c.m2l_off[k], ri);
+      }
+    }
+  }
+  std::vector<int64_t> pos(f->n_points);
+  for (int64_t i = 0; i < f->n_points; ++i) pos[i] = i;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t x = 0; x < nc; ++x) {
+    const int64_t nx = f->cl_end[x] - f->cl_start[x];
+    for (int64_t k = f->near_rowptr[x]; k < f->near_rowptr[x + 1]; ++k) {
+      if (!f->near_off || f->near_off[k] < 0) continue;
+      const int64_t y = f->near_src[k];
+      const int64_t ny = f->cl_end[y] - f->cl_start[y];
+      if (f->near_off[k] + nx * ny > blob_len) {
+#pragma omp critical
+        err = "near block out of blob";
+        continue;
+      }
+      K.block_cm(pos.data() + f->cl_start[x], nx, pos.data() + f->cl_start[y], ny,
+                 blob + f->near_off[k], nx);
+    }
+  }
+  if (!err.empty()) {
+    g_err = err;
+    return H2B_ERR_INVALID_ARG;
+  }
+  return H2B_OK;
+}
 const char* h2b_last_error(void) { return g_err.c_str(); }
 
 int h2b_build(const h2b_params* params, h2b_result** out) {

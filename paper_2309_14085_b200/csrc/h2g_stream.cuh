@@ -360,6 +360,10 @@ constexpr int kMmaMinCols = H2G_MMA_MIN_COLS;      // columns per chunk at least
 #define H2G_MMA_GROUP_MIN 2
 #endif
 constexpr bool kMmaGroupMode = H2G_MMA_GROUP != 0;  // wide phases in group mode
+#ifndef H2G_MMA_DUAL
+#define H2G_MMA_DUAL 1
+#endif
+constexpr bool kMmaDualAcc = H2G_MMA_DUAL != 0;     // two accumulator sets for short row groups
 constexpr int kMmaGroupMin = H2G_MMA_GROUP_MIN;     // smallest group (warps per chunk stream)
 constexpr int kChunkAMmaTall = H2G_MMA_CHUNK_TALL;  // chunk of group-mode phases with tasks
                                                      // taller than 64 rows
@@ -401,17 +405,47 @@ __device__ __forceinline__ void mma_step(const double (&a)[TPW], const double (&
 // One chunk for one warp: tiles i < TPW at rows 8 (w_r + wr i), k-steps
 // w_k, w_k + wk, ...  Ab: lane's A element of (tile 0, k-step 0); Bb: lane's
 // X element of (k-step 0, plane 0); xps: smem plane stride.
+// Short row groups (TPW <= 4 tiles: TPW x NT <= 8 accumulator chains) leave
+// the DMMA pipe waiting on its own results (ncu: "wait" stalls); they
+// alternate k-steps between two accumulator sets (c: even, c2: odd), summed
+// in that fixed order at the task's end.
 template <int TPW, int NT>
 __device__ __forceinline__ void consume_mma(const double* __restrict__ Ab, int ldas, int tstride,
                                             const double* __restrict__ Bb, int xps, int ncols,
-                                            int kq, int w_k, int wk, double (&c)[8][2][2]) {
+                                            int kq, int w_k, int wk, double (&c)[8][2][2],
+                                            double (&c2)[4][2][2]) {
   const int full = ncols >> 2;                 // whole k-steps
   const int n_my = full > w_k ? (full - w_k + wk - 1) / wk : 0;
   const int adv_a = 4 * ldas * wk, adv_b = 4 * 8 * wk;
   const double* Ap = Ab + 4 * ldas * w_k;
   const double* Bp = Bb + 4 * 8 * w_k;
+  int t = 0;
+  if constexpr (TPW <= 4 && kMmaDualAcc) {
+    for (; t + 2 <= n_my; t += 2) {
+      double a[TPW], b[NT], a2[TPW], b2[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        b[nt] = Bp[nt * xps];
+        b2[nt] = Bp[adv_b + nt * xps];
+      }
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        a[i] = Ap[i * tstride];
+        a2[i] = Ap[adv_a + i * tstride];
+      }
+#pragma unroll
+      for (int i = 0; i < TPW; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma(c[i][nt], a[i], b[nt]);
+          dmma(c2[i][nt], a2[i], b2[nt]);
+        }
+      Ap += 2 * adv_a;
+      Bp += 2 * adv_b;
+    }
+  }
 #pragma unroll 2
-  for (int t = 0; t < n_my; ++t) {
+  for (; t < n_my; ++t) {
     double a[TPW], b[NT];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) b[nt] = Bp[nt * xps];
@@ -551,10 +585,26 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
     cls_k[k] = cw / wr;
   }
   double c[8][2][2];
+  double c2[4][2][2];  // odd k-steps of short row groups (consume_mma)
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) c[i][nt][0] = c[i][nt][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) c2[i][nt][0] = c2[i][nt][1] = 0.0;
+  // fold the odd-k-step accumulators into c (fixed order) and clear them
+  auto fold_c2 = [&]() {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        c[i][nt][0] += c2[i][nt][0];
+        c[i][nt][1] += c2[i][nt][1];
+        c2[i][nt][0] = c2[i][nt][1] = 0.0;
+      }
+  };
   if (group > 0) {
     // GROUP mode: warps [G st, G st + G) own chunk stream st (chunks i = st
     // mod S); warp g of the group takes row tiles g, g + G, ... (<= 8, the
@@ -585,17 +635,17 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
         const int xps = 8 * ncols;
         const int ts = 8 * G;
         switch (tpw) {
-          case 1: consume_mma<1, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
-          case 2: consume_mma<2, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
-          case 3: consume_mma<3, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
-          case 4: consume_mma<4, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
+          case 1: consume_mma<1, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c, c2); break;
+          case 2: consume_mma<2, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c, c2); break;
+          case 3: consume_mma<3, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c, c2); break;
+          case 4: consume_mma<4, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c, c2); break;
           default:
             if constexpr (kMaxTpw > 4) {
               switch (tpw) {
-                case 5: consume_mma<5, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
-                case 6: consume_mma<6, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
-                case 7: consume_mma<7, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
-                default: consume_mma<8, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c); break;
+                case 5: consume_mma<5, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c, c2); break;
+                case 6: consume_mma<6, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c, c2); break;
+                case 7: consume_mma<7, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c, c2); break;
+                default: consume_mma<8, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, 0, 1, c, c2); break;
               }
             }
             break;
@@ -604,6 +654,7 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (flags & kLastOfTask) {
+        fold_c2();
         double* y = arena + y_off * 8;
 #pragma unroll
         for (int t = 0; t < kMaxTpw; ++t) {
@@ -655,17 +706,17 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
       const int xps = 8 * ncols;
       const int ts = 8 * wr;
       switch (tpw) {
-        case 1: consume_mma<1, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
-        case 2: consume_mma<2, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
-        case 3: consume_mma<3, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
-        case 4: consume_mma<4, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
+        case 1: consume_mma<1, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c, c2); break;
+        case 2: consume_mma<2, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c, c2); break;
+        case 3: consume_mma<3, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c, c2); break;
+        case 4: consume_mma<4, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c, c2); break;
         default:
           if constexpr (kMaxTpw > 4) {
             switch (tpw) {
-              case 5: consume_mma<5, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
-              case 6: consume_mma<6, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
-              case 7: consume_mma<7, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
-              default: consume_mma<8, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c); break;
+              case 5: consume_mma<5, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c, c2); break;
+              case 6: consume_mma<6, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c, c2); break;
+              case 7: consume_mma<7, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c, c2); break;
+              default: consume_mma<8, NT>(Ab, ldas, ts, Bb, xps, ncols, kq, w_k, wk, c, c2); break;
             }
           }
           break;
@@ -674,6 +725,7 @@ stream_mma_kernel(const ChunkRec* __restrict__ recs, const int64_t* __restrict__
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (flags & kLastOfTask) {
+      fold_c2();
       double* y = arena + y_off * 8;  // plane 0; plane nt at + nt * ps
       // classes with wk > 1 have at most 4 tiles per warp
       if (wk > 1) {  // park partials of column groups 1.. ; group 0 combines them

@@ -125,3 +125,54 @@ def test_unstored_blocks_build(store):
         assert (ch.m2l_off < 0).all() == ("m2l" not in store)
     assert len(sop.blob) < len(nop.blob)
     assert rel_err(packed_matvec(sop, z["q"]), packed_matvec(nop, z["q"])) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["g3d_lap_k3_h2plusH", "g2d_cfg1_h2star", "g3d_gauss_k3_h2star"])
+def test_materialize_blocks_is_the_stored_build(name):
+    """h2b_fill_kernel_blocks re-evaluates the blocks a store="" build (or a
+    compact reference fixture) left out: bitwise the blocks a stored build
+    holds; against the reference's numpy blocks bitwise for 1/r (sqrt and
+    division are correctly rounded) and to the last ulp for log / exp (libm
+    vs numpy's vectorised log / exp)."""
+    from golden_io import materialize
+    from paper_2309_14085_b200.builder import materialize_blocks
+    op, z, meta = load_golden(name)
+    exact = meta["kernel"] == "lap3d"
+
+    def same(a, b):
+        if exact:
+            return np.array_equal(a, b)
+        return np.max(np.abs(a - b), initial=0.0) <= 4e-16 * np.max(np.abs(b), initial=0.0)
+
+    full = materialize_blocks(op)
+    assert (full.near_off >= 0).all() and all((c.m2l_off >= 0).all() for c in full.channels)
+    ref = materialize(op)  # oracle re-evaluation, same offsets order per block
+    for k in range(0, len(op.near_src), 5):
+        x = np.searchsorted(op.near_rowptr, k, side="right") - 1
+        y = op.near_src[k]
+        a = full.mat(full.near_off[k], op.size(x), op.size(y))
+        b = ref.mat(ref.near_off[k], op.size(x), op.size(y))
+        assert same(a, b)
+    ch, cr = full.channels[0], ref.channels[0]
+    for k in range(0, len(ch.m2l_src), 7):
+        x = np.searchsorted(ch.m2l_rowptr, k, side="right") - 1
+        y = ch.m2l_src[k]
+        assert same(full.mat(ch.m2l_off[k], ch.r_in[x], ch.r_out[y]),
+                    ref.mat(cr.m2l_off[k], ch.r_in[x], ch.r_out[y]))
+    assert rel_err(packed_matvec(full, z["q"]), z["phi_ref"]) <= 1e-13
+    nat = build_variant(meta["variant"], _pts(op), kernel=meta["kernel"], n_max=meta["n_max"],
+                        eps=meta["eps"], store="")
+    nfull = materialize_blocks(nat)
+    nst = build_variant(meta["variant"], _pts(op), kernel=meta["kernel"], n_max=meta["n_max"],
+                        eps=meta["eps"])
+    for k in range(0, len(nst.near_src), 11):
+        x = np.searchsorted(nst.near_rowptr, k, side="right") - 1
+        y = nst.near_src[k]
+        assert np.array_equal(nst.mat(nst.near_off[k], nst.size(x), nst.size(y)),
+                              nfull.mat(nfull.near_off[k], nst.size(x), nst.size(y)))
+
+
+def _pts(op):
+    pts = np.empty_like(op.points_tree)
+    pts[op.perm] = op.points_tree
+    return pts

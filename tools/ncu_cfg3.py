@@ -1,21 +1,24 @@
 """ncu evidence for bench.py's cfg-3 roofline (one GPU).
 
-    python tools/ncu_cfg3.py build /tmp/cfg3     # native build -> mmap-able export dir
+    python tools/ncu_cfg3.py build /tmp/cfg3     # native build (store="") -> export dir
     python tools/ncu_cfg3.py run /tmp/cfg3       # plain run: must exit 0 first
     ncu --set full --clock-control none --import-source on \
-        -k regex:"stream_gemv|p2p_tasks" -s 32 -c 16 -o gpurun_out/prof_cfg3 \
+        -k regex:"stream_gemv|p2p_tasks" -s 32 -c 31 -o /tmp/prof_cfg3 \
         python tools/ncu_cfg3.py run /tmp/cfg3
-    python tools/ncu_cfg3.py summarize gpurun_out/prof_cfg3.ncu-rep [out_dir]
+    python tools/ncu_cfg3.py summarize /tmp/prof_cfg3.ncu-rep [out_dir]
 
-(the export directory keeps the profiled command under ncu's 300 s plain-run
-limit: the native build happens once, before.)  The export is BASELINE
-configs[2] with its M2L blocks not stored (the headline plan evaluates them;
-the plan is the bench's, whose stored M2L blocks never leave the host), so it
-fits the box's disk.  The run does 3 matvecs of the headline plan (16
-filtered launches each); with -s 32 -c 16 ncu captures the third.
-``summarize`` writes profiles/traffic_cfg3_h2star-bt_eval.json (DRAM bytes
-of the headline matvec) and profiles/p2p_cfg3_h2star-bt.json (fp64-pipe
-utilisation of the P2P launches, time-weighted).
+The NCA pivot search (minutes) runs once, in ``build``, which exports
+BASELINE configs[2] with only the transfer operators, pivots and points
+(~1 GB); ``run`` re-evaluates the M2L / near blocks natively
+(builder.materialize_blocks: bitwise the blocks of a stored build, seconds),
+so the profiled command stays under ncu's 300 s plain-run limit.  It then
+does 3 matvecs of the bench's headline plan (M2L evaluated at
+bench.M2L_EVAL_SHARE, 16 filtered launches each) and 1 matvec of the
+all-streamed plan (15 launches); -s 32 -c 31 captures the third headline
+matvec and the streamed one.  ``summarize`` writes
+traffic_cfg3_h2star-bt_eval.json / traffic_cfg3_h2star-bt.json (DRAM bytes
+per matvec) and p2p_cfg3_h2star-bt.json (fp64-pipe utilisation of the P2P
+launches, time-weighted).
 """
 import csv
 import io
@@ -37,20 +40,29 @@ METRICS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 def build(path):
     from paper_2309_14085_b200.builder import build_variant, uniform_points
     op = build_variant("h2star-bt", uniform_points(1 << 20, 3, 42), "lap3d", 64, 1e-6,
-                       store="near")
+                       store="")
     op.save_dir(path)
 
 
 def run(path):
+    import time
     import numpy as np
+    sys.path.insert(0, ROOT)
+    from bench import M2L_EVAL_SHARE
+    from paper_2309_14085_b200.builder import materialize_blocks
     from paper_2309_14085_b200.gpu_rep import GpuHierRep
     from paper_2309_14085_b200.packed import PackedOperator
-    op = PackedOperator.load_dir(path)
+    t0 = time.time()
+    op = materialize_blocks(PackedOperator.load_dir(path))  # = the stored build, bitwise
+    print("materialized in", time.time() - t0, "s")
     q = np.random.default_rng(43).standard_normal(op.N)
-    with GpuHierRep(op, recompute="m2l") as rep:
+    with GpuHierRep(op, recompute="m2l", m2l_share=M2L_EVAL_SHARE) as rep:
         for _ in range(3):
             rep.matvec(q)
         print("headline launches per matvec", rep.launches_per_matvec())
+    with GpuHierRep(op) as rep:
+        rep.matvec(q)
+        print("streamed launches per matvec", rep.launches_per_matvec())
 
 
 def _rows(rep_path):
@@ -84,14 +96,16 @@ def summarize(rep_path, n_head=16, out_dir=None):
     tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
     def t(r):
         return _f(r, "gpu__time_duration.sum") * tscale.get(units.get("gpu__time_duration.sum"), 1e-9)
-    head = rows[:n_head]
+    head, stream = rows[:n_head], rows[n_head:]
     out_dir = out_dir or os.path.join(ROOT, "profiles")
     os.makedirs(out_dir, exist_ok=True)
-    for name, rr in (("traffic_cfg3_h2star-bt_eval.json", head),):
+    for name, rr in (("traffic_cfg3_h2star-bt_eval.json", head),
+                     ("traffic_cfg3_h2star-bt.json", stream)):
         rd = sum(by(r, "dram__bytes_read.sum") for r in rr)
         wr = sum(by(r, "dram__bytes_write.sum") for r in rr)
         out = {"config": "cfg3", "variant": "h2star-bt", "launches": len(rr),
-               "mode": "M2L evaluated" if rr is head else "all streamed",
+               "mode": ("M2L evaluated (share 0.7; 0.3 TMA-staged in the P2P tasks)"
+                        if rr is head else "all streamed"),
                "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
                "kernel_time_s_serialised": sum(t(r) for r in rr),
                "per_launch": [{"kernel": r.get("Kernel Name", "")[:60], "us": t(r) * 1e6,

@@ -43,7 +43,7 @@ def main():
             check(f"{name} pinned graph", out, z["phi_ref"])
         os.environ["H2G_MMA_GROUP_MIN_TASKS"] = "1"
         with GpuHierRep(op) as rep:
-            check(f"{name} dmma group", rep.matmat(z["Q"].repeat(4, axis=1))[:, 1], z["Phi_ref"][:, 1])
+            check(f"{name} dmma group", rep.matmat(np.tile(z["Q"], (1, 4)))[:, 1], z["Phi_ref"][:, 1])
         os.environ.pop("H2G_MMA_GROUP_MIN_TASKS")
         with GpuHierRep(op, recompute="near,m2l") as rep:
             check(f"{name} p2p", rep.matvec(z["q"]), z["phi_ref"])
