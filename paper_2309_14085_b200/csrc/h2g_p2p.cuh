@@ -104,7 +104,11 @@ __device__ __forceinline__ void issue_stage(const P2PStage& st, double* slot, ui
   bulk_g2s(slot, reinterpret_cast<const void*>(st.src), st.bytes, bar);
 }
 
-template <int KT, int DIM, int L, int J>
+// FULL: the phase has self blocks (near diagonal) or coincident points (the
+// r == 0 test in every entry); M2L phases of distinct points run the plain
+// evaluation loop only -- a third of the code (the dispatch instantiates
+// every L x J layout, and instruction fetch was a top stall at the leaf level).
+template <int KT, int DIM, int L, int J, bool FULL>
 __device__ __forceinline__ void p2p_task(const P2PTask& tk, const Term* __restrict__ terms,
                                          const P2PChunk* __restrict__ chunks,
                                          const P2PStage* __restrict__ stages,
@@ -205,7 +209,7 @@ __device__ __forceinline__ void p2p_task(const P2PTask& tk, const Term* __restri
         nx = arena[cd.x_off + lane];
       }
     }
-    if (self) {
+    if (FULL && self) {
       for (int c = g; c < n; c += G) {
         const double4 s = srec[buf][c];
         const double xv = sx[buf][c];
@@ -219,7 +223,7 @@ __device__ __forceinline__ void p2p_task(const P2PTask& tk, const Term* __restri
           acc[j] = fma(kv, xv, acc[j]);
         }
       }
-    } else if (kp.check) {
+    } else if (FULL && kp.check) {
 #pragma unroll 2
       for (int c = g; c < n; c += G) {
         const double4 s = srec[buf][c];
@@ -296,7 +300,7 @@ __device__ __forceinline__ void p2p_task(const P2PTask& tk, const Term* __restri
 #endif
 constexpr int kP2PRowsPerLane = H2G_P2P_JT;
 
-template <int KT, int DIM>
+template <int KT, int DIM, bool FULL>
 __device__ __forceinline__ void p2p_dispatch(const P2PTask& tk, const Term* __restrict__ terms,
                                              const P2PChunk* __restrict__ chunks,
                                              const P2PStage* __restrict__ stages,
@@ -312,7 +316,7 @@ __device__ __forceinline__ void p2p_dispatch(const P2PTask& tk, const Term* __re
   while (L < 32 && L * JT < m) L <<= 1;
   const int J = (m + L - 1) / L;
 #define H2G_P2P(Lv, Jv)                                                                     \
-  p2p_task<KT, DIM, Lv, Jv>(tk, terms, chunks, stages, recs, blob, arena, kp, srec, sx, red, \
+  p2p_task<KT, DIM, Lv, Jv, FULL>(tk, terms, chunks, stages, recs, blob, arena, kp, srec, sx, red, \
                             slots, sbar, sphase, lane, warp)
 #define H2G_P2P_J(Lv)                                                  \
   switch (J) {                                                         \
@@ -342,7 +346,7 @@ __device__ __forceinline__ void p2p_dispatch(const P2PTask& tk, const Term* __re
 // host sorts them); the last CTA to leave resets the counters for the next
 // launch (graph replays reuse them).  Counters schedule work only: every
 // output is written once, in a fixed summation order.
-template <int KT, int DIM>
+template <int KT, int DIM, bool FULL>
 __global__ void __launch_bounds__(kP2PThreads, kP2PCtasPerSm)
 p2p_tasks_kernel(const P2PTask* __restrict__ tasks, int n_tasks, const Term* __restrict__ terms,
                  const P2PChunk* __restrict__ chunks, const P2PStage* __restrict__ stages,
@@ -369,7 +373,7 @@ p2p_tasks_kernel(const P2PTask* __restrict__ tasks, int n_tasks, const Term* __r
     const int t = *s_task;
     if (t >= n_tasks) break;
     const P2PTask tk = tasks[t];
-    p2p_dispatch<KT, DIM>(tk, terms, chunks, stages, recs, blob, arena, kp, srec[warp], sx[warp],
+    p2p_dispatch<KT, DIM, FULL>(tk, terms, chunks, stages, recs, blob, arena, kp, srec[warp], sx[warp],
                           red, slots, sbar, sphase, lane, warp);
     __syncthreads();  // red / s_task reuse
   }

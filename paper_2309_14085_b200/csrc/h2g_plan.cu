@@ -85,6 +85,7 @@ struct Phase {
   // run CONCURRENTLY on two graph branches over disjoint targets, so the HBM
   // and the fp64 pipe are busy at once
   int32_t hybrid = 0;
+  int32_t p2p_full = 0;  // some P2P chunk of the phase is a self block (near diagonal)
 };
 
 // Multi-GPU ownership: subtrees at level `level` are split into
@@ -586,6 +587,7 @@ void build_p2p_lists(const HostSchedule& s, std::vector<Phase>& phases,
           pterms.push_back(tm);
           continue;
         }
+        if (tm.pad) ph.p2p_full = 1;
         for (int32_t c0 = 0; c0 < tm.ncols; c0 += kP2PChunk) {
           P2PChunk c;
           c.x_off = tm.x_off + c0;
@@ -1338,11 +1340,22 @@ int launch_p2p(h2g_plan* p, const Phase& ph, int phase_idx, cudaStream_t s, bool
   const P2PTask* tk = p->d_p2p_tasks + ph.p2p_off;
   int* ctr = p->d_ctr + 2 * phase_idx;
   const int kt = p->kernel_type, d3 = p->dim >= 3;
+  const bool full = ph.p2p_full || p->kp.check;  // self blocks / coincident points
 #define H2G_LAUNCH_P2P(KT, DIM)                                                              \
-  CUDA_TRY(launch_k(p->pdl && pdl, p2p_tasks_kernel<KT, DIM>, grid, kP2PThreads, kP2PSmem, s, tk, \
-                    (int)n, (const Term*)p->d_p2p_terms, (const P2PChunk*)p->d_p2p_chunks,     \
-                    (const P2PStage*)p->d_p2p_stages, (const double4*)p->d_recs4,             \
-                    (const double*)p->d_blob, p->d_arena, p->kp, ctr))
+  do {                                                                                       \
+    if (full)                                                                                \
+      CUDA_TRY(launch_k(p->pdl && pdl, p2p_tasks_kernel<KT, DIM, true>, grid, kP2PThreads,   \
+                        kP2PSmem, s, tk, (int)n, (const Term*)p->d_p2p_terms,                \
+                        (const P2PChunk*)p->d_p2p_chunks, (const P2PStage*)p->d_p2p_stages,  \
+                        (const double4*)p->d_recs4, (const double*)p->d_blob, p->d_arena,    \
+                        p->kp, ctr));                                                        \
+    else                                                                                     \
+      CUDA_TRY(launch_k(p->pdl && pdl, p2p_tasks_kernel<KT, DIM, false>, grid, kP2PThreads,  \
+                        kP2PSmem, s, tk, (int)n, (const Term*)p->d_p2p_terms,                \
+                        (const P2PChunk*)p->d_p2p_chunks, (const P2PStage*)p->d_p2p_stages,  \
+                        (const double4*)p->d_recs4, (const double*)p->d_blob, p->d_arena,    \
+                        p->kp, ctr));                                                        \
+  } while (0)
   if (kt == 0) {
     if (d3) H2G_LAUNCH_P2P(0, 3); else H2G_LAUNCH_P2P(0, 2);
   } else if (kt == 1) {
@@ -1771,11 +1784,14 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kStreamSmem));
     // P2P kernels: maximum shared-memory carve-out (L1 is not what they need)
-#define H2G_P2P_CARVEOUT(KT, DIM)                                                       \
-  CUDA_TRY(cudaFuncSetAttribute(p2p_tasks_kernel<KT, DIM>,                              \
+#define H2G_P2P_CARVEOUT1(KT, DIM, F)                                                   \
+  CUDA_TRY(cudaFuncSetAttribute(p2p_tasks_kernel<KT, DIM, F>,                           \
                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100));  \
-  CUDA_TRY(cudaFuncSetAttribute(p2p_tasks_kernel<KT, DIM>,                              \
+  CUDA_TRY(cudaFuncSetAttribute(p2p_tasks_kernel<KT, DIM, F>,                           \
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2PSmem))
+#define H2G_P2P_CARVEOUT(KT, DIM) \
+  H2G_P2P_CARVEOUT1(KT, DIM, true);  \
+  H2G_P2P_CARVEOUT1(KT, DIM, false)
     H2G_P2P_CARVEOUT(0, 2);
     H2G_P2P_CARVEOUT(0, 3);
     H2G_P2P_CARVEOUT(1, 2);
@@ -1783,6 +1799,7 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     H2G_P2P_CARVEOUT(2, 2);
     H2G_P2P_CARVEOUT(2, 3);
 #undef H2G_P2P_CARVEOUT
+#undef H2G_P2P_CARVEOUT1
     CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<8>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem));
     CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<16>,

@@ -361,7 +361,7 @@ constexpr int kMmaMinCols = H2G_MMA_MIN_COLS;      // columns per chunk at least
 #endif
 constexpr bool kMmaGroupMode = H2G_MMA_GROUP != 0;  // wide phases in group mode
 #ifndef H2G_MMA_DUAL
-#define H2G_MMA_DUAL 1
+#define H2G_MMA_DUAL 0  // measured: no gain at cfg 2 (1.958 -> 1.973 ms per 16 RHS)
 #endif
 constexpr bool kMmaDualAcc = H2G_MMA_DUAL != 0;     // two accumulator sets for short row groups
 constexpr int kMmaGroupMin = H2G_MMA_GROUP_MIN;     // smallest group (warps per chunk stream)

@@ -66,8 +66,11 @@ def run(path):
 
 
 def _rows(rep_path):
-    out = subprocess.run(["ncu", "-i", rep_path, "--page", "raw", "--csv"], check=True,
-                         capture_output=True, text=True).stdout
+    if rep_path.endswith(".csv"):  # an `ncu -i ... --page raw --csv` dump
+        out = open(rep_path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep_path, "--page", "raw", "--csv"], check=True,
+                             capture_output=True, text=True).stdout
     lines = out.splitlines()
     rd = csv.reader(io.StringIO("\n".join(lines)))
     hdr = next(rd)
@@ -90,10 +93,12 @@ def _f(r, k):
 
 def summarize(rep_path, n_head=16, out_dir=None):
     rows, units = _rows(rep_path)
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6,
+             "GB": 1e9}
     def by(r, k):
         return _f(r, k) * scale.get(units.get(k, "byte"), 1)
-    tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
+    tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9,
+              "us": 1e-6, "ms": 1e-3, "s": 1.0}
     def t(r):
         return _f(r, "gpu__time_duration.sum") * tscale.get(units.get("gpu__time_duration.sum"), 1e-9)
     head, stream = rows[:n_head], rows[n_head:]
