@@ -1,0 +1,168 @@
+// Microbenchmark of the P2P (kernel-evaluation) engine on synthetic task
+// lists shaped like config 3's M2L levels:
+//   l5: 32768 targets, ~32 rows, ~119 blocks of ~32 columns   (leaf level)
+//   l4:  4096 targets, ~113 rows, ~93 blocks of ~113 columns
+// A share 1 - s of every target's block entries is stored (TMA-staged from a
+// blob far larger than L2), the rest evaluated (1/r, 3D).  Runs the real
+// kernel of csrc/h2g_p2p.cuh; compile-time variants through -D macros:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
+//        --expt-relaxed-constexpr -I include -o ubench_p2p tools/ubench_p2p.cu
+//   ./ubench_p2p l5 0.7
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#ifdef UB_OLD
+#include "h2g_p2p_old.cuh"
+#else
+#include "../paper_2309_14085_b200/csrc/h2g_p2p.cuh"
+#endif
+
+using namespace h2g;
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) {                                                         \
+      fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_));     \
+      exit(1);                                                                       \
+    }                                                                                \
+  } while (0)
+
+__global__ void fill(double* p, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v * (double)((i * 2654435761ull) % 1024) / 1024.0;
+}
+
+int main(int argc, char** argv) {
+  const char* level = argc > 1 ? argv[1] : "l5";
+  const double share = argc > 2 ? atof(argv[2]) : 1.0;
+  const int reps = argc > 3 ? atoi(argv[3]) : 5;
+  int T, m_lo, m_hi, nb, c_lo, c_hi;
+  if (!strcmp(level, "l5")) {
+    T = 32768; m_lo = 24; m_hi = 40; nb = 119; c_lo = 24; c_hi = 40;
+  } else if (!strcmp(level, "l4")) {
+    T = 4096; m_lo = 100; m_hi = 126; nb = 93; c_lo = 100; c_hi = 126;
+  } else {  // l5x: exact 32 x 32 blocks
+    T = 32768; m_lo = 32; m_hi = 32; nb = 119; c_lo = 32; c_hi = 32;
+  }
+  std::mt19937_64 rng(7);
+  auto uni = [&](int lo, int hi) { return lo + (int)(rng() % (uint64_t)(hi - lo + 1)); };
+  const int64_t n_rec = 1 << 22, n_arena = (1 << 23) + (int64_t)T * 256;
+  const int64_t y_base = 1 << 23;
+  std::vector<P2PTask> tasks;
+  std::vector<P2PChunk> chunks;
+  std::vector<P2PStage> stages;
+  double* d_blob = nullptr;
+  const size_t blob_doubles = (size_t)12 << 27;  // 12 GiB
+  CK(cudaMalloc(&d_blob, blob_doubles * 8));
+  fill<<<148 * 8, 256>>>(d_blob, blob_doubles, 1e-3);
+  size_t boff = 0;
+  double n_eval = 0, n_stream = 0;
+  for (int t = 0; t < T; ++t) {
+    P2PTask q{};
+    q.m = uni(m_lo, m_hi);
+    q.y_off = y_base + (int64_t)t * 256;
+    q.row_rec = (int32_t)(rng() % (uint64_t)(n_rec / 2 - 256));  // rows: first half of the records
+    q.k_begin = (int32_t)chunks.size();
+    q.s_begin = (int32_t)stages.size();
+    double tot = 0, str = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int nc = uni(c_lo, c_hi);
+      const int64_t x_off = (int64_t)(rng() % (uint64_t)((1 << 23) - 256));
+      const double e = (double)q.m * nc;
+      tot += e;
+      if (share < 1.0 && str + e <= (1.0 - share) * tot + 0.5 * e) {  // error diffusion
+        str += e;
+        n_stream += e;
+        if (boff + (size_t)q.m * nc + 2 > blob_doubles) boff = 0;
+#ifdef UB_OLD
+        const int64_t cc = std::max<int64_t>(1, (kP2PStageBytes - 16) / (8 * (int64_t)q.m));
+        for (int64_t c0 = 0; c0 < nc; c0 += cc) {
+          const int64_t n1 = std::min<int64_t>(cc, nc - c0);
+          const uint64_t src = reinterpret_cast<uint64_t>(d_blob + boff + c0 * q.m);
+          const uint64_t a = src & ~uint64_t(15);
+          const uint64_t en = (src + 8ull * (uint64_t)(q.m * n1) + 15) & ~uint64_t(15);
+          P2PStage st{};
+          st.src = a; st.x_off = x_off + c0; st.bytes = (uint32_t)(en - a);
+          st.ncols = (int16_t)n1; st.shift = (int16_t)((src - a) / 8);
+          stages.push_back(st);
+        }
+#else
+        p2p_cut_stages(d_blob + boff, q.m, nc, x_off, stages);
+#endif
+        boff += (size_t)q.m * nc;
+        continue;
+      }
+      n_eval += e;
+      const int32_t rec = (int32_t)(n_rec / 2 + rng() % (uint64_t)(n_rec / 2 - 256));  // columns: second half
+      for (int c0 = 0; c0 < nc; c0 += kP2PChunk) {
+        P2PChunk c;
+        c.x_off = x_off + c0;
+        c.rec = rec + c0;
+        c.n_self = std::min(kP2PChunk, nc - c0);
+        chunks.push_back(c);
+      }
+    }
+    q.k_end = (int32_t)chunks.size();
+    q.s_end = (int32_t)stages.size();
+    tasks.push_back(q);
+  }
+  std::vector<double4> recs(n_rec);
+  std::uniform_real_distribution<double> U(-1.0, 1.0);
+  for (auto& r : recs) r = make_double4(U(rng), U(rng), U(rng), 0.0);
+  P2PTask* d_tasks; P2PChunk* d_chunks; P2PStage* d_stages; double4* d_recs; double* d_arena; int* d_ctr;
+  Term* d_terms;
+  CK(cudaMalloc(&d_tasks, tasks.size() * sizeof(P2PTask)));
+  CK(cudaMalloc(&d_chunks, (chunks.size() + 1) * sizeof(P2PChunk)));
+  CK(cudaMalloc(&d_stages, (stages.size() + 1) * sizeof(P2PStage)));
+  CK(cudaMalloc(&d_recs, recs.size() * sizeof(double4)));
+  CK(cudaMalloc(&d_arena, (n_arena + 8) * 8));
+  CK(cudaMalloc(&d_ctr, 8));
+  CK(cudaMalloc(&d_terms, 64));
+  CK(cudaMemcpy(d_tasks, tasks.data(), tasks.size() * sizeof(P2PTask), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_chunks, chunks.data(), chunks.size() * sizeof(P2PChunk), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_stages, stages.data(), stages.size() * sizeof(P2PStage), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_recs, recs.data(), recs.size() * sizeof(double4), cudaMemcpyHostToDevice));
+  CK(cudaMemset(d_ctr, 0, 8));
+  fill<<<148 * 8, 256>>>(d_arena, n_arena, 1.0);
+  CK(cudaDeviceSynchronize());
+  P2PKernel kp{};
+  auto kfn = p2p_tasks_kernel<1, 3, false>;
+  CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2PSmem));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kP2PThreads, kP2PSmem));
+  const unsigned grid = 148 * kP2PCtasPerSm;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  float best = 1e30f, sum = 0;
+  for (int r = 0; r < reps + 2; ++r) {
+    CK(cudaEventRecord(e0));
+    kfn<<<grid, kP2PThreads, kP2PSmem>>>(d_tasks, T, d_terms, d_chunks, d_stages, d_recs, d_blob,
+                                          d_arena, kp, d_ctr);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaGetLastError());
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (r >= 2) { best = std::min(best, ms); sum += ms; }
+  }
+  // checksum of the outputs (identical across layout variants up to summation order)
+  std::vector<double> y((size_t)T * 256);
+  CK(cudaMemcpy(y.data(), d_arena + y_base, y.size() * 8, cudaMemcpyDeviceToHost));
+  double cs = 0;
+  for (int t = 0; t < T; ++t)
+    for (int r = 0; r < tasks[t].m; ++r) cs += y[(size_t)t * 256 + r];
+  const double ms = sum / reps;
+  printf("{\"level\": \"%s\", \"share\": %.2f, \"ms\": %.4f, \"best_ms\": %.4f, \"occ\": %d, "
+         "\"eval_entries\": %.4g, \"stream_entries\": %.4g, \"eval_Tps\": %.4f, \"stream_GBps\": %.1f, "
+         "\"total_Tps\": %.4f, \"stages\": %zu, \"chunks\": %zu, \"checksum\": %.12e}\n",
+         level, share, ms, best, occ, n_eval, n_stream, n_eval / ms / 1e9, 8 * n_stream / ms / 1e6,
+         (n_eval + n_stream) / ms / 1e9, stages.size(), chunks.size(), cs);
+  return 0;
+}
