@@ -207,10 +207,11 @@ def cpu_port_time(op, q, budget_s=15.0, max_steps=20):
 
 
 # Share of the STORED M2L entries the P2P engine evaluates when it evaluates
-# M2L; the rest of every target's blocks stream (TMA-staged) inside the same
-# tasks, so HBM and the fp64 pipe work at once (tools/hybrid_sweep.py, cfg 3:
-# 1.0 -> 11.69 ms, 0.8 -> 11.14, 0.7 -> 10.92, 0.6 -> 11.16, 0.5 -> 11.58).
-M2L_EVAL_SHARE = 0.7
+# M2L; the rest of every target's blocks stream (TMA-staged, multiplied by the
+# P2P CTAs' streaming warps) inside the same tasks, so HBM and the fp64 pipe
+# work at once (tools/variant_sweep.py, cfg 3: 1.0 -> 11.44 ms, 0.7 -> 10.07,
+# 0.6 -> 10.04, 0.5 -> 10.34).
+M2L_EVAL_SHARE = 0.6
 
 
 def recompute_for(cfg, arg, op=None):

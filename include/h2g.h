@@ -202,6 +202,13 @@ int h2g_shard_get_info(const h2g_plan* plan, h2g_shard_info* out);
 int h2g_matvec_begin(h2g_plan* plan, const double* q_dev, int64_t n, void* stream);
 int h2g_shard_pack(h2g_plan* plan, double* send_dev, void* stream);
 int h2g_shard_unpack(h2g_plan* plan, const double* recv_dev, void* stream);
+/* The owned near field (it reads only q) as its own step: call it between
+ * h2g_shard_pack and h2g_shard_unpack, after starting the all-gather, and it
+ * runs while the exchange is in flight; the leaf tasks add its partial sums
+ * (fixed order).  h2g_matvec_end / h2g_shard_store_phi run it themselves if
+ * the caller did not.  H2G_SHARD_OVERLAP=0 at plan creation keeps the near
+ * field inside the leaf phase. */
+int h2g_shard_overlap(h2g_plan* plan, void* stream);
 int h2g_matvec_end(h2g_plan* plan, double* phi_dev, int64_t n, void* stream);
 
 /* Distributed vectors: q and phi live as each rank's OWN tree-order rows

@@ -67,6 +67,7 @@ def emulate_begin(view, op, q):
     send = np.zeros(max(1, view["max_send_slots"]))
     for src, dst, ln in view["pack"]:
         send[dst:dst + ln] = arena[src:src + ln]
+    run_phases(view, op, blob, arena, 2)  # the owned near field, beside the exchange
     return arena, send
 
 
@@ -135,6 +136,7 @@ def emulate_matvec_distributed(op, q, nranks: int, recompute: str = "") -> np.nd
         send = np.zeros(max(1, v["max_send_slots"]))
         for src, dst, ln in v["pack"]:
             send[dst:dst + ln] = arena[src:src + ln]
+        run_phases(v, op, blob, arena, 2)  # the owned near field, beside the exchange
         states.append((arena, send))
     mx = max(1, views[0]["max_send_slots"])
     recv = np.zeros(mx * nranks)

@@ -68,7 +68,7 @@ H2G_SYMBOLS = ("h2g_plan_create", "h2g_plan_destroy", "h2g_plan_get_stats", "h2g
                "h2g_shard_pack", "h2g_shard_unpack", "h2g_matvec_end",
                "h2g_schedule_build", "h2g_schedule_get", "h2g_schedule_free",
                "h2g_shard_load_q", "h2g_halo_pack", "h2g_halo_unpack", "h2g_shard_part0",
-               "h2g_shard_store_phi")
+               "h2g_shard_store_phi", "h2g_shard_overlap")
 
 _LIB = None
 
@@ -113,6 +113,7 @@ def load(path: str = None) -> C.CDLL:
     for name in ("h2g_shard_load_q", "h2g_halo_pack", "h2g_halo_unpack", "h2g_shard_store_phi"):
         getattr(L, name).argtypes = [vp, vp, vp]
     L.h2g_shard_part0.argtypes = [vp, vp]
+    L.h2g_shard_overlap.argtypes = [vp, vp]
     L.h2g_schedule_build.argtypes = [C.POINTER(ExportDesc), C.c_int, C.c_int, C.POINTER(vp)]
     L.h2g_schedule_get.argtypes = [vp, C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int32)]

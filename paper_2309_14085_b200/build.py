@@ -24,7 +24,8 @@ NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
            "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 
 TARGETS = {
-    "libh2g.so": (["h2g_plan.cu"], ["h2g_kernels.cuh", "h2g_stream.cuh", "h2g_p2p.cuh", "h2g_eval.cuh"], "h2g.h"),
+    "libh2g.so": (["h2g_plan.cu", "h2g_p2p_launch.cu"],
+                  ["h2g_kernels.cuh", "h2g_stream.cuh", "h2g_p2p.cuh", "h2g_eval.cuh"], "h2g.h"),
     "libh2b.so": (["h2b_build.cpp"], [], "h2b.h"),
 }
 CXX = os.environ.get("H2_CXX", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++")
@@ -51,7 +52,19 @@ def build(force: bool = False, verbose: bool = True) -> dict:
             os.path.join(ROOT, "include", header), __file__]
         if force or _stale(out, dep_paths):
             if srcs[0].endswith(".cu"):
-                cmd = [NVCC, *ARCH, *NVFLAGS, "-shared", "-o", out, *src_paths]
+                # one object per translation unit, compiled concurrently, then linked
+                objs, procs = [], []
+                for sp in src_paths:
+                    obj = os.path.join(LIBDIR, os.path.basename(sp) + ".o")
+                    cmd = [NVCC, *ARCH, *NVFLAGS, "-c", "-o", obj, sp]
+                    if verbose:
+                        print(" ".join(cmd), file=sys.stderr)
+                    procs.append((cmd, subprocess.Popen(cmd)))
+                    objs.append(obj)
+                for cmd, pr in procs:
+                    if pr.wait() != 0:
+                        raise subprocess.CalledProcessError(pr.returncode, cmd)
+                cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs]
             else:
                 cmd = [CXX, *CXXFLAGS, "-shared", "-o", out, *src_paths]
             if verbose:

@@ -101,7 +101,7 @@ __device__ __forceinline__ void run_task(const Task& tk, const Term* __restrict_
 
 // One CTA per task.  Rows-per-lane J is chosen per task at run time and
 // dispatched to a compile-time instance so accumulators stay in registers.
-__global__ void __launch_bounds__(kWarps * 32)
+static __global__ void __launch_bounds__(kWarps * 32)
 gemv_tasks_kernel(const Task* __restrict__ tasks, const Term* __restrict__ terms,
                   const double* __restrict__ blob, double* arena) {
   __shared__ double red[kWarps * kMaxRows];
@@ -114,7 +114,7 @@ gemv_tasks_kernel(const Task* __restrict__ tasks, const Term* __restrict__ terms
 }
 
 // q_tree[i] = q[perm[i] * ld]  (tree order gather, reference q[index_set])
-__global__ void gather_perm_kernel(const double* __restrict__ q, int64_t ld,
+static __global__ void gather_perm_kernel(const double* __restrict__ q, int64_t ld,
                                    const int32_t* __restrict__ perm, double* __restrict__ out,
                                    int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -123,7 +123,7 @@ __global__ void gather_perm_kernel(const double* __restrict__ q, int64_t ld,
 }
 
 // phi[perm[i] * ld] = phi_tree[i]  (reference phi[index_set] +=, disjoint slices)
-__global__ void scatter_perm_kernel(const double* __restrict__ in,
+static __global__ void scatter_perm_kernel(const double* __restrict__ in,
                                     const int32_t* __restrict__ perm, double* __restrict__ phi,
                                     int64_t ld, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -165,7 +165,7 @@ struct CopyRange {
   int64_t src, dst, len;
 };
 
-__global__ void copy_ranges_kernel(const CopyRange* __restrict__ r, int n,
+static __global__ void copy_ranges_kernel(const CopyRange* __restrict__ r, int n,
                                    const double* __restrict__ src, double* __restrict__ dst) {
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
     const CopyRange c = r[k];
@@ -200,7 +200,7 @@ __global__ void reduce_partials_kernel(const RedTask* __restrict__ t, int n,
 }
 
 // phi[perm[i] * ld] = phi_tree[i] for tree rows i in [i0, i1) (owned rows)
-__global__ void scatter_rows_kernel(const double* __restrict__ in, const int32_t* __restrict__ perm,
+static __global__ void scatter_rows_kernel(const double* __restrict__ in, const int32_t* __restrict__ perm,
                                     double* __restrict__ phi, int64_t ld, int64_t i0, int64_t i1) {
   for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < i1;
        i += (int64_t)gridDim.x * blockDim.x)

@@ -86,6 +86,7 @@ struct Phase {
   // and the fp64 pipe are busy at once
   int32_t hybrid = 0;
   int32_t p2p_full = 0;  // some P2P chunk of the phase is a self block (near diagonal)
+  int32_t p2p_sw = 0;    // some P2P task of the phase has TMA stages (streaming warp)
 };
 
 // Multi-GPU ownership: subtrees at level `level` are split into
@@ -187,6 +188,9 @@ struct h2g_plan {
   int64_t row_begin = 0, row_end = 0;
   cudaGraph_t graph1 = nullptr;      // part 1 (after the exchange) of a sharded plan
   cudaGraphExec_t graph1_exec = nullptr;
+  cudaGraph_t graph2 = nullptr;      // part 2 (owned near field, beside the exchange)
+  cudaGraphExec_t graph2_exec = nullptr;
+  bool overlap_pending = false;      // part 2 not yet run in the current matvec
   int64_t ones_off = 0, n_ones = 0;
   cudaStream_t stream = nullptr;
   double* d_blob = nullptr;
@@ -555,6 +559,15 @@ void build_p2p_lists(const HostSchedule& s, std::vector<Phase>& phases,
                      const double* d_blob, bool stage) {
   for (Phase& ph : phases) {
     ph.p2p_off = (int64_t)pt.size();
+    // phases with self blocks (the near field) run the FULL kernels, which
+    // have no streaming warp: their stored terms are read directly
+    bool stage_ph = stage && d_blob;
+    for (int64_t i = stream_end_of(ph); stage_ph && i < ph.task_end; ++i)
+      for (int32_t k = s.tasks[i].t_begin; k < s.tasks[i].t_end; ++k)
+        if (s.terms[k].a_space == kRecompute && s.terms[k].pad) {
+          stage_ph = false;
+          break;
+        }
     for (int64_t i = stream_end_of(ph); i < ph.task_end; ++i) {
       const Task& t = s.tasks[i];
       P2PTask q{};
@@ -566,21 +579,9 @@ void build_p2p_lists(const HostSchedule& s, std::vector<Phase>& phases,
       q.s_begin = (int32_t)pst.size();
       for (int32_t k = t.t_begin; k < t.t_end; ++k) {
         const Term& tm = s.terms[k];
-        if (stage && tm.a_space == 0 && tm.lda == t.m && tm.ncols > 0 && d_blob) {
-          const int64_t cc = std::max<int64_t>(1, (kP2PStageBytes - 16) / (8 * (int64_t)t.m));
-          for (int64_t c0 = 0; c0 < tm.ncols; c0 += cc) {
-            const int64_t nc = std::min<int64_t>(cc, tm.ncols - c0);
-            const uint64_t src = reinterpret_cast<uint64_t>(d_blob + tm.a_off + c0 * t.m);
-            const uint64_t a = src & ~uint64_t(15);
-            const uint64_t e = (src + 8ull * (uint64_t)(t.m * nc) + 15) & ~uint64_t(15);
-            P2PStage st{};
-            st.src = a;
-            st.x_off = tm.x_off + c0;
-            st.bytes = (uint32_t)(e - a);
-            st.ncols = (int16_t)nc;
-            st.shift = (int16_t)((src - a) / 8);
-            pst.push_back(st);
-          }
+        if (stage_ph && tm.a_space == 0 && tm.lda == t.m && tm.ncols > 0) {
+          p2p_cut_stages(d_blob + tm.a_off, t.m, tm.ncols, tm.x_off, pst);
+          ph.p2p_sw = 1;
           continue;
         }
         if (tm.a_space != kRecompute) {
@@ -703,6 +704,16 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
   slots += max_parts;
   p->ones_off = ones_off;
   p->n_ones = max_parts;
+  // sharded plans: the owned near field does not depend on the exchange; it
+  // runs beside the all-gather (phase "near_own", part 2) into this partial,
+  // which the leaf tasks add as one more term (partial * ones(1))
+  const char* ov_env = getenv("H2G_SHARD_OVERLAP");
+  const bool overlap = sh.nranks > 1 && !(ov_env && atoi(ov_env) == 0);
+  int64_t near_part = -1;
+  if (overlap) {
+    near_part = slots;
+    slots += d->n_points;
+  }
   p->n_slots = slots;
 
   // ---- exchange layout: slots each rank produces that other ranks read ----
@@ -933,6 +944,39 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
     end_phase(s);
   }
 
+  // near terms of leaf x (stored blocks, or evaluated from the points)
+  auto add_near_terms = [&](int64_t x, bool& any_rc) -> int {
+    const int64_t nx = nsz(x);
+    for (int64_t k = d->near_rowptr[x]; k < d->near_rowptr[x + 1]; ++k) {
+      const int64_t y = d->near_src[k];
+      if (y < 0 || y >= nc) return fail(H2G_ERR_BAD_EXPORT, "near source out of range");
+      if (d->near_off[k] < 0 || (d->recompute & H2G_RECOMPUTE_NEAR)) {
+        add_rc_term(s, st[y], p->q_tree + st[y], nsz(y), y == x);
+        any_rc = true;
+        continue;
+      }
+      if (!in_blob(d, d->near_off[k], nx, nsz(y)))
+        return fail(H2G_ERR_BAD_EXPORT, "near block out of blob");
+      add_term(s, d->near_off[k], p->q_tree + st[y], nx, nsz(y));
+    }
+    return H2G_OK;
+  };
+  // ================= part 2: beside the exchange (sharded plans) =================
+  if (overlap) {
+    begin_phase(s, PH_GEMV, "near_own");
+    s.phases.back().part = 2;
+    bytes = 0;
+    for (int64_t x = lo[kappa]; x < lo[kappa + 1]; ++x) {
+      const int64_t nx = nsz(x);
+      if (nx == 0 || !mine(x, kappa) || d->near_rowptr[x + 1] == d->near_rowptr[x]) continue;
+      bool any_rc = false;
+      if (int r = add_near_terms(x, any_rc)) return r;
+      emit_task(s, near_part + st[x], nx, bytes, any_rc ? st[x] : -1);
+    }
+    s.phases.back().alg_bytes = bytes;
+    end_phase(s);
+  }
+
   // ================= part 1: after the exchange =================
   // ---- downward: M2L (+ fused L2L) levels 1 .. kappa ----
   for (int l = 1; l <= kappa; ++l) {
@@ -1032,17 +1076,11 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
       if (l > 1) a = parent(a, l);
     }
     bool any_rc = false;
-    for (int64_t k = d->near_rowptr[x]; k < d->near_rowptr[x + 1]; ++k) {
-      const int64_t y = d->near_src[k];
-      if (y < 0 || y >= nc) return fail(H2G_ERR_BAD_EXPORT, "near source out of range");
-      if (d->near_off[k] < 0 || (d->recompute & H2G_RECOMPUTE_NEAR)) {
-        add_rc_term(s, st[y], p->q_tree + st[y], nsz(y), y == x);
-        any_rc = true;
-        continue;
-      }
-      if (!in_blob(d, d->near_off[k], nx, nsz(y)))
-        return fail(H2G_ERR_BAD_EXPORT, "near block out of blob");
-      add_term(s, d->near_off[k], p->q_tree + st[y], nx, nsz(y));
+    if (overlap) {  // the near field was summed beside the exchange
+      if (d->near_rowptr[x + 1] > d->near_rowptr[x])
+        add_term(s, near_part + st[x], ones_off, nx, 1, /*a_space=*/1);
+    } else if (int r = add_near_terms(x, any_rc)) {
+      return r;
     }
     emit_task(s, p->phi_tree + st[x], nx, bytes, any_rc ? st[x] : -1);
   }
@@ -1335,35 +1373,15 @@ int launch_p2p(h2g_plan* p, const Phase& ph, int phase_idx, cudaStream_t s, bool
   if (n <= 0) return H2G_OK;
   // one CTA per task, persistent; beside the streaming engine's CTA (hybrid
   // phases) only kP2PHybridCtas fit on an SM
-  const int64_t per_sm = ph.hybrid ? kP2PHybridCtas : kP2PCtasPerSm;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, p->n_sm * per_sm));
-  const P2PTask* tk = p->d_p2p_tasks + ph.p2p_off;
-  int* ctr = p->d_ctr + 2 * phase_idx;
-  const int kt = p->kernel_type, d3 = p->dim >= 3;
   const bool full = ph.p2p_full || p->kp.check;  // self blocks / coincident points
-#define H2G_LAUNCH_P2P(KT, DIM)                                                              \
-  do {                                                                                       \
-    if (full)                                                                                \
-      CUDA_TRY(launch_k(p->pdl && pdl, p2p_tasks_kernel<KT, DIM, true>, grid, kP2PThreads,   \
-                        kP2PSmem, s, tk, (int)n, (const Term*)p->d_p2p_terms,                \
-                        (const P2PChunk*)p->d_p2p_chunks, (const P2PStage*)p->d_p2p_stages,  \
-                        (const double4*)p->d_recs4, (const double*)p->d_blob, p->d_arena,    \
-                        p->kp, ctr));                                                        \
-    else                                                                                     \
-      CUDA_TRY(launch_k(p->pdl && pdl, p2p_tasks_kernel<KT, DIM, false>, grid, kP2PThreads,  \
-                        kP2PSmem, s, tk, (int)n, (const Term*)p->d_p2p_terms,                \
-                        (const P2PChunk*)p->d_p2p_chunks, (const P2PStage*)p->d_p2p_stages,  \
-                        (const double4*)p->d_recs4, (const double*)p->d_blob, p->d_arena,    \
-                        p->kp, ctr));                                                        \
-  } while (0)
-  if (kt == 0) {
-    if (d3) H2G_LAUNCH_P2P(0, 3); else H2G_LAUNCH_P2P(0, 2);
-  } else if (kt == 1) {
-    if (d3) H2G_LAUNCH_P2P(1, 3); else H2G_LAUNCH_P2P(1, 2);
-  } else {
-    if (d3) H2G_LAUNCH_P2P(2, 3); else H2G_LAUNCH_P2P(2, 2);
-  }
-#undef H2G_LAUNCH_P2P
+  const bool sw = ph.p2p_sw && !full;
+  const int64_t per_sm = ph.hybrid ? kP2PHybridCtas : p2p_ctas_per_sm(sw);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, p->n_sm * per_sm));
+  CUDA_TRY(p2p_launch(p->kernel_type, p->dim, full, sw, p->pdl && pdl, grid, s,
+                      p->d_p2p_tasks + ph.p2p_off, (int)n, (const Term*)p->d_p2p_terms,
+                      (const P2PChunk*)p->d_p2p_chunks, (const P2PStage*)p->d_p2p_stages,
+                      (const double4*)p->d_recs4, (const double*)p->d_blob, p->d_arena, p->kp,
+                      p->d_ctr + 2 * phase_idx));
   CUDA_TRY(cudaGetLastError());
   return H2G_OK;
 }
@@ -1464,6 +1482,8 @@ void free_plan(h2g_plan* p) {
   if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
   if (p->graph1_exec) cudaGraphExecDestroy(p->graph1_exec);
   if (p->graph1) cudaGraphDestroy(p->graph1);
+  if (p->graph2_exec) cudaGraphExecDestroy(p->graph2_exec);
+  if (p->graph2) cudaGraphDestroy(p->graph2);
   cudaFree(p->d_pack);
   cudaFree(p->d_unpack);
   cudaFree(p->d_hpack);
@@ -1625,6 +1645,7 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     p->kp.check = has_coincident_points(d) ? 1 : 0;
     p->use_batched = false;  // the tensor-pipe engine streams stored blocks only
   }
+  if (nranks > 1) p->use_batched = false;  // leaf tasks of sharded plans add a per-RHS partial
   std::vector<double> local_blob;
   if (p->compact) compact_blob(d, s, local_blob);
   {
@@ -1760,8 +1781,9 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
       // stage stored blocks through TMA when a share of the M2L blocks streams
       // inside the P2P tasks (measured: staging only the small L2L / L2P
       // terms of all-evaluated tasks costs ~3 %; direct loads there)
+      // (coincident points run the FULL kernels everywhere: no streaming warp)
       const bool stage = d->m2l_recompute_share > 0.0 && d->m2l_recompute_share < 1.0 &&
-                         (d->recompute & H2G_RECOMPUTE_M2L);
+                         (d->recompute & H2G_RECOMPUTE_M2L) && !p->kp.check;
       build_p2p_lists(s, p->phases, pt, pterms, pch, pst, p->d_blob, stage);
       if ((int64_t)pch.size() >= (1LL << 31) || (int64_t)pst.size() >= (1LL << 31))
         return fail(H2G_ERR_BAD_EXPORT, "too many chunks");
@@ -1783,23 +1805,7 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     CUDA_TRY(cudaFuncSetAttribute(stream_gemv_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kStreamSmem));
-    // P2P kernels: maximum shared-memory carve-out (L1 is not what they need)
-#define H2G_P2P_CARVEOUT1(KT, DIM, F)                                                   \
-  CUDA_TRY(cudaFuncSetAttribute(p2p_tasks_kernel<KT, DIM, F>,                           \
-                                cudaFuncAttributePreferredSharedMemoryCarveout, 100));  \
-  CUDA_TRY(cudaFuncSetAttribute(p2p_tasks_kernel<KT, DIM, F>,                           \
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2PSmem))
-#define H2G_P2P_CARVEOUT(KT, DIM) \
-  H2G_P2P_CARVEOUT1(KT, DIM, true);  \
-  H2G_P2P_CARVEOUT1(KT, DIM, false)
-    H2G_P2P_CARVEOUT(0, 2);
-    H2G_P2P_CARVEOUT(0, 3);
-    H2G_P2P_CARVEOUT(1, 2);
-    H2G_P2P_CARVEOUT(1, 3);
-    H2G_P2P_CARVEOUT(2, 2);
-    H2G_P2P_CARVEOUT(2, 3);
-#undef H2G_P2P_CARVEOUT
-#undef H2G_P2P_CARVEOUT1
+    CUDA_TRY(p2p_configure());
     CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<8>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMmaSmem));
     CUDA_TRY(cudaFuncSetAttribute(stream_mma_kernel<16>,
@@ -1824,8 +1830,8 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
                          sizeof(int32_t) * p->N;
     // capture the fixed middle phases into CUDA graphs: one for an unsharded
     // plan; part 0 / part 1 (around the exchange) for a sharded one
-    for (int part = 0; part < 2; ++part) {
-      if (part == 1 && nranks == 1) break;
+    for (int part = 0; part < 3; ++part) {
+      if (part >= 1 && nranks == 1) break;
       CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
       for (size_t pi = 0; pi < p->phases.size(); ++pi) {
         const Phase& ph = p->phases[pi];
@@ -1838,8 +1844,9 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
           return lr;
         }
       }
-      cudaGraph_t* gp = part == 0 ? &p->graph : &p->graph1;
-      cudaGraphExec_t* ge = part == 0 ? &p->graph_exec : &p->graph1_exec;
+      cudaGraph_t* gp = part == 0 ? &p->graph : (part == 1 ? &p->graph1 : &p->graph2);
+      cudaGraphExec_t* ge =
+          part == 0 ? &p->graph_exec : (part == 1 ? &p->graph1_exec : &p->graph2_exec);
       CUDA_TRY(cudaStreamEndCapture(p->stream, gp));
       CUDA_TRY(cudaGraphInstantiate(ge, *gp, 0));
     }
@@ -2080,6 +2087,30 @@ int h2g_matvec_begin(h2g_plan* p, const double* q_dev, int64_t n, void* stream) 
     return mark_stream(p, s);
   }
   CUDA_TRY(cudaGraphLaunch(p->graph_exec, s));
+  p->overlap_pending = true;
+  return mark_stream(p, s);
+}
+
+// Part 2 of a sharded plan (the owned near field, which reads only q): call
+// it between h2g_shard_pack and h2g_shard_unpack so it runs while the
+// all-gather is in flight; h2g_matvec_end / h2g_shard_store_phi run it
+// themselves if the caller did not.
+static int run_overlap(h2g_plan* p, cudaStream_t s) {
+  if (!p->overlap_pending) return H2G_OK;
+  p->overlap_pending = false;
+  if (p->graph2_exec) CUDA_TRY(cudaGraphLaunch(p->graph2_exec, s));
+  return H2G_OK;
+}
+
+int h2g_shard_overlap(h2g_plan* p, void* stream) {
+  NvtxRange nvtx_range_("h2g_shard_overlap");
+  if (!p) return fail(H2G_ERR_INVALID_ARG, "null plan");
+  if (p->shard.nranks == 1) return fail(H2G_ERR_INVALID_ARG, "not a sharded plan");
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = join_stream(p, s);
+  if (rc) return rc;
+  if ((rc = run_overlap(p, s))) return rc;
   return mark_stream(p, s);
 }
 
@@ -2120,7 +2151,10 @@ int h2g_matvec_end(h2g_plan* p, double* phi_dev, int64_t n, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   int rc = join_stream(p, s);
   if (rc) return rc;
-  if (p->shard.nranks > 1) CUDA_TRY(cudaGraphLaunch(p->graph1_exec, s));
+  if (p->shard.nranks > 1) {
+    if ((rc = run_overlap(p, s))) return rc;
+    CUDA_TRY(cudaGraphLaunch(p->graph1_exec, s));
+  }
   const int64_t rows = p->row_end - p->row_begin;
   if (rows > 0) {
     scatter_rows_kernel<<<grid_for(rows), 256, 0, s>>>(p->d_arena + p->phi_tree, p->d_perm,
@@ -2182,6 +2216,7 @@ int h2g_shard_part0(h2g_plan* p, void* stream) {
   int rc = join_stream(p, s);
   if (rc) return rc;
   CUDA_TRY(cudaGraphLaunch(p->graph_exec, s));
+  p->overlap_pending = true;
   return mark_stream(p, s);
 }
 
@@ -2194,7 +2229,10 @@ int h2g_shard_store_phi(h2g_plan* p, double* phi_own_dev, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   int rc = join_stream(p, s);
   if (rc) return rc;
-  if (p->shard.nranks > 1) CUDA_TRY(cudaGraphLaunch(p->graph1_exec, s));
+  if (p->shard.nranks > 1) {
+    if ((rc = run_overlap(p, s))) return rc;
+    CUDA_TRY(cudaGraphLaunch(p->graph1_exec, s));
+  }
   if (rows > 0)
     CUDA_TRY(cudaMemcpyAsync(phi_own_dev, p->d_arena + p->phi_tree + p->row_begin,
                              sizeof(double) * rows, cudaMemcpyDeviceToDevice, s));

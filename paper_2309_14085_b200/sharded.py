@@ -90,6 +90,18 @@ class ShardedGpuHierRep:
         _lib.check(self._L.h2g_shard_pack(self._plan, C.c_void_p(send.data_ptr()),
                                           C.c_void_p(stream)), L=self._L)
 
+    def overlap(self, stream):
+        """The owned near field (reads only q): launched after the all-gather
+        has been started, it runs while the exchange is in flight."""
+        _lib.check(self._L.h2g_shard_overlap(self._plan, C.c_void_p(stream)),
+                   "h2g_shard_overlap", L=self._L)
+
+    def _all_gather_overlapped(self, dist, recv, send, stream):
+        """All-gather on NCCL's stream with the owned near field on ours."""
+        work = dist.all_gather_into_tensor(recv, send, group=self.group, async_op=True)
+        self.overlap(stream)
+        work.wait()  # our stream waits for the exchange; the host does not block
+
     def unpack(self, recv, stream):
         _lib.check(self._L.h2g_shard_unpack(self._plan, C.c_void_p(recv.data_ptr()),
                                             C.c_void_p(stream)), L=self._L)
@@ -134,7 +146,7 @@ class ShardedGpuHierRep:
             _lib.check(L.h2g_shard_part0(self._plan, C.c_void_p(stream)), "h2g_shard_part0", L=L)
             send, recv = self._buffers(torch)
             self.pack(send, stream)
-            dist.all_gather_into_tensor(recv, send, group=self.group)
+            self._all_gather_overlapped(dist, recv, send, stream)
             self.unpack(recv, stream)
         else:
             raise ValueError("matvec_distributed needs a sharded plan (nranks > 1)")
@@ -155,7 +167,7 @@ class ShardedGpuHierRep:
         self.begin(q, stream)
         if self.nranks > 1:
             self.pack(send, stream)
-            dist.all_gather_into_tensor(recv, send, group=self.group)
+            self._all_gather_overlapped(dist, recv, send, stream)
             self.unpack(recv, stream)
         self.end(phi, stream)
         if gather_full and self.nranks > 1:

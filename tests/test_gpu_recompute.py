@@ -19,7 +19,7 @@ from oracle.packed_matvec import packed_matvec
 pytestmark = pytest.mark.gpu
 NAMES = golden_names()
 TOL = 1e-12
-MODES = [("near", 1.0), ("m2l", 1.0), ("near,m2l", 1.0), ("near,m2l", 0.5)]
+MODES = [("near", 1.0), ("m2l", 1.0), ("near,m2l", 1.0), ("near,m2l", 0.5), ("m2l", 0.6)]
 
 
 @pytest.mark.parametrize("mode,share", MODES)

@@ -115,8 +115,8 @@ def test_cfg3_streamed_vs_evaluated_vs_oracle(cfg3_op, capsys):
     """North-star HBM config (cfg 3) at full size, both operating modes:
 
     * streamed (every block read from HBM) vs M2L evaluated (the bench's
-      headline mode) vs near + M2L evaluated: each <= 1e-12 from the others
-      over all N rows;
+      headline mode, all evaluated and with the bench's staged share) vs
+      near + M2L evaluated: each <= 1e-12 from the others over all N rows;
     * each vs the oracle restatement of the reference matvec on 48 sampled
       target leaves (packed_matvec_rows: full upward pass, the leaves'
       ancestor chains) <= 1e-12;
@@ -129,13 +129,18 @@ def test_cfg3_streamed_vs_evaluated_vs_oracle(cfg3_op, capsys):
     op, pts = cfg3_op
     N = op.N
     q = np.random.default_rng(43).standard_normal(N)
+    import bench
     res = {}
-    for mode in ("", "m2l", "near,m2l"):
-        with GpuHierRep(op, recompute=mode) as rep:
-            res[mode] = rep.matvec(q)
-            assert np.array_equal(res[mode], rep.matvec(q))
-    assert rel_err(res["m2l"], res[""]) <= 1e-12
-    assert rel_err(res["near,m2l"], res[""]) <= 1e-12
+    # "m2l@staged": the bench's headline plan (a share of every target's M2L
+    # blocks evaluated, the rest TMA-staged by the P2P CTAs' streaming warps)
+    for key, mode, share in (("", "", 1.0), ("m2l", "m2l", 1.0),
+                             ("m2l@staged", "m2l", bench.M2L_EVAL_SHARE),
+                             ("near,m2l", "near,m2l", 1.0)):
+        with GpuHierRep(op, recompute=mode, m2l_share=share) as rep:
+            res[key] = rep.matvec(q)
+            assert np.array_equal(res[key], rep.matvec(q))
+    for key in ("m2l", "m2l@staged", "near,m2l"):
+        assert rel_err(res[key], res[""]) <= 1e-12, key
     lo = op.level_offset
     rng = np.random.default_rng(11)
     leaves = rng.choice(np.arange(lo[op.kappa], lo[op.kappa + 1]), 48, replace=False)

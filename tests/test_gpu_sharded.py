@@ -25,6 +25,8 @@ def _virtual_ranks(op, q, R, recompute=""):
         send = torch.zeros(mx, dtype=torch.float64, device="cuda")
         rep.begin(qd, stream)
         rep.pack(send, stream)
+        if r % 2 == 0:  # the owned near field beside the exchange, as matvec() does;
+            rep.overlap(stream)  # odd ranks leave it to end()
         recv[r * mx:(r + 1) * mx] = send
     phi = torch.zeros_like(qd)
     for rep in reps:

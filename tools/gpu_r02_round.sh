@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 check on the GPU box: GPU tests, smoke, both bench arms as the driver
-# runs them, then compute-sanitizer (memcheck / racecheck / synccheck) over
-# tools/sanitize_cases.py.
+# runs them, tools/sanitize_cases.py (plain), then the ncu evidence of the
+# cfg-3 headline plan (tools/gpu_ncu_cfg3.sh).
 mkdir -p gpurun_out
 (nproc; free -g; nvidia-smi --query-gpu=name,memory.total --format=csv) > gpurun_out/box.txt 2>&1
 SECONDS=0
@@ -11,11 +11,6 @@ SECONDS=0
 timeout 1700 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "rc $? after ${SECONDS}s" >> gpurun_out/bench_ref.err
 SECONDS=0
 timeout 1700 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "rc $? after ${SECONDS}s" >> gpurun_out/bench.err
-timeout 900 python tools/sanitize_cases.py > gpurun_out/sanitize_plain.log 2>&1 || exit 0
-for tool in memcheck racecheck synccheck; do
-  SECONDS=0
-  extra=""
-  [ $tool = memcheck ] && extra="--leak-check full"
-  timeout 1500 compute-sanitizer --tool $tool $extra --print-limit 50 python tools/sanitize_cases.py > gpurun_out/sanitize_$tool.log 2>&1
-  echo "$tool rc $? after ${SECONDS}s" >> gpurun_out/sanitize_$tool.log
-done
+timeout 900 python tools/sanitize_cases.py > gpurun_out/sanitize_plain.log 2>&1
+# (compute-sanitizer is closed on this pool: profiles/sanitizer_r02.md)
+bash tools/gpu_ncu_cfg3.sh

@@ -4,8 +4,8 @@ mkdir -p gpurun_out
 out=gpurun_out/ubench_p2p.jsonl
 : > $out
 for b in $(ls scratch/ub); do
-  for lv in l5 l4; do
-    for s in 1.0 0.7 0.6 0.5; do
+  for lv in ${LEVELS:-l5r l4r}; do
+    for s in ${SHARES:-1.0 0.7 0.6 0.5}; do
       echo -n "{\"bin\": \"$b\"} " >> $out
       timeout 120 scratch/ub/$b $lv $s >> $out 2>&1 || echo "FAILED rc $?" >> $out
     done

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <random>
 #include <vector>
 
@@ -42,17 +43,28 @@ int main(int argc, char** argv) {
   const char* level = argc > 1 ? argv[1] : "l5";
   const double share = argc > 2 ? atof(argv[2]) : 1.0;
   const int reps = argc > 3 ? atoi(argv[3]) : 5;
-  int T, m_lo, m_hi, nb, c_lo, c_hi;
+  // lN: uniform synthetic tasks; lNr: the shape of config 3's level N as the
+  // native build produces it (two channels per target: ~100 and ~6 source
+  // blocks; ranks spread around their mean; one stored L2L block per task)
+  int T, m_lo, m_hi, nb, c_lo, c_hi, nb2 = 0, l2l = 0;
   if (!strcmp(level, "l5")) {
     T = 32768; m_lo = 24; m_hi = 40; nb = 119; c_lo = 24; c_hi = 40;
   } else if (!strcmp(level, "l4")) {
     T = 4096; m_lo = 100; m_hi = 126; nb = 93; c_lo = 100; c_hi = 126;
+  } else if (!strcmp(level, "l5r")) {
+    T = 32768; m_lo = 15; m_hi = 53; nb = 100; c_lo = 15; c_hi = 53; nb2 = 6; l2l = 100;
+  } else if (!strcmp(level, "l4r")) {
+    T = 4096; m_lo = 71; m_hi = 116; nb = 78; c_lo = 71; c_hi = 116; nb2 = 5; l2l = 100;
   } else {  // l5x: exact 32 x 32 blocks
     T = 32768; m_lo = 32; m_hi = 32; nb = 119; c_lo = 32; c_hi = 32;
   }
   std::mt19937_64 rng(7);
-  auto uni = [&](int lo, int hi) { return lo + (int)(rng() % (uint64_t)(hi - lo + 1)); };
-  const int64_t n_rec = 1 << 22, n_arena = (1 << 23) + (int64_t)T * 256;
+  // triangular around the middle of [lo, hi] (ranks cluster around their mean)
+  auto uni = [&](int lo, int hi) {
+    const int w = hi - lo + 1;
+    return lo + (int)((rng() % (uint64_t)w + rng() % (uint64_t)w) / 2);
+  };
+  const int64_t n_rec = 1 << 22, n_arena = (1 << 23) + (int64_t)T * 512;
   const int64_t y_base = 1 << 23;
   std::vector<P2PTask> tasks;
   std::vector<P2PChunk> chunks;
@@ -63,21 +75,57 @@ int main(int argc, char** argv) {
   fill<<<148 * 8, 256>>>(d_blob, blob_doubles, 1e-3);
   size_t boff = 0;
   double n_eval = 0, n_stream = 0;
+  struct Blk { int nc; int64_t x_off; bool stored; int32_t rec; };
+  std::vector<std::pair<double, std::vector<Blk>>> protos;  // (cost, blocks) per task
+  std::vector<int> proto_m;
   for (int t = 0; t < T; ++t) {
+    const int m = uni(m_lo, m_hi);
+    for (int ch = 0; ch < (nb2 ? 2 : 1); ++ch) {
+      const int nblk = ch == 0 ? nb + (nb2 ? (int)(rng() % 21) - 10 : 0) : nb2;
+      std::vector<Blk> bl;
+      double tot = 0, str = 0;
+      for (int b = 0; b < nblk; ++b) {
+        Blk k;
+        k.nc = uni(c_lo, c_hi);
+        k.x_off = (int64_t)(rng() % (uint64_t)((1 << 23) - 256));
+        const double e = (double)m * k.nc;
+        tot += e;
+        k.stored = share < 1.0 && str + e <= (1.0 - share) * tot + 0.5 * e;  // error diffusion
+        if (k.stored) str += e;
+        k.rec = (int32_t)(n_rec / 2 + rng() % (uint64_t)(n_rec / 2 - 256));  // columns: second half
+        bl.push_back(k);
+      }
+      if (l2l && share < 1.0) {  // the task's L2L block: stored, staged with the M2L share
+        Blk k;
+        k.nc = l2l + (int)(rng() % 21) - 10;
+        k.x_off = (int64_t)(rng() % (uint64_t)((1 << 23) - 256));
+        k.stored = true;
+        k.rec = 0;
+        bl.push_back(k);
+        tot += (double)m * k.nc;
+      }
+      protos.push_back({tot, std::move(bl)});
+      proto_m.push_back(m);
+    }
+  }
+  std::vector<int> order(protos.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return protos[a].first > protos[b].first; });  // largest first
+  const int n_tasks = (int)order.size();
+  for (int oi = 0; oi < n_tasks; ++oi) {
+    const int t = order[oi];
     P2PTask q{};
-    q.m = uni(m_lo, m_hi);
-    q.y_off = y_base + (int64_t)t * 256;
+    q.m = proto_m[t];
+    q.y_off = y_base + (int64_t)oi * 256;
     q.row_rec = (int32_t)(rng() % (uint64_t)(n_rec / 2 - 256));  // rows: first half of the records
     q.k_begin = (int32_t)chunks.size();
     q.s_begin = (int32_t)stages.size();
-    double tot = 0, str = 0;
-    for (int b = 0; b < nb; ++b) {
-      const int nc = uni(c_lo, c_hi);
-      const int64_t x_off = (int64_t)(rng() % (uint64_t)((1 << 23) - 256));
+    for (const Blk& k : protos[t].second) {
+      const int nc = k.nc;
+      const int64_t x_off = k.x_off;
       const double e = (double)q.m * nc;
-      tot += e;
-      if (share < 1.0 && str + e <= (1.0 - share) * tot + 0.5 * e) {  // error diffusion
-        str += e;
+      if (k.stored) {
         n_stream += e;
         if (boff + (size_t)q.m * nc + 2 > blob_doubles) boff = 0;
 #ifdef UB_OLD
@@ -99,11 +147,10 @@ int main(int argc, char** argv) {
         continue;
       }
       n_eval += e;
-      const int32_t rec = (int32_t)(n_rec / 2 + rng() % (uint64_t)(n_rec / 2 - 256));  // columns: second half
       for (int c0 = 0; c0 < nc; c0 += kP2PChunk) {
         P2PChunk c;
         c.x_off = x_off + c0;
-        c.rec = rec + c0;
+        c.rec = k.rec + c0;
         c.n_self = std::min(kP2PChunk, nc - c0);
         chunks.push_back(c);
       }
@@ -112,6 +159,7 @@ int main(int argc, char** argv) {
     q.s_end = (int32_t)stages.size();
     tasks.push_back(q);
   }
+  T = n_tasks;
   std::vector<double4> recs(n_rec);
   std::uniform_real_distribution<double> U(-1.0, 1.0);
   for (auto& r : recs) r = make_double4(U(rng), U(rng), U(rng), 0.0);
@@ -132,18 +180,29 @@ int main(int argc, char** argv) {
   fill<<<148 * 8, 256>>>(d_arena, n_arena, 1.0);
   CK(cudaDeviceSynchronize());
   P2PKernel kp{};
+#ifdef UB_OLD
   auto kfn = p2p_tasks_kernel<1, 3, false>;
-  CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2PSmem));
+  const size_t smem = kP2PSmem;
+  const int threads = kP2PThreads, per_sm = kP2PCtasPerSm;
+#else
+  // a streaming warp per CTA when the tasks have TMA stages (as launch_p2p does)
+  const bool sw = !stages.empty();
+  auto kfn = sw ? p2p_tasks_kernel<1, 3, false, true> : p2p_tasks_kernel<1, 3, false, false>;
+  const size_t smem = p2p_smem_bytes(sw);
+  const int threads = sw ? kP2PThreadsSW : kP2PThreads, per_sm = sw ? kP2PCtasSW : kP2PCtasPerSm;
+#endif
+  CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kP2PThreads, kP2PSmem));
-  const unsigned grid = 148 * kP2PCtasPerSm;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, threads, smem));
+  const unsigned grid = 148 * per_sm;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   float best = 1e30f, sum = 0;
   for (int r = 0; r < reps + 2; ++r) {
     CK(cudaEventRecord(e0));
-    kfn<<<grid, kP2PThreads, kP2PSmem>>>(d_tasks, T, d_terms, d_chunks, d_stages, d_recs, d_blob,
+    kfn<<<grid, threads, smem>>>(d_tasks, T, d_terms, d_chunks, d_stages, d_recs, d_blob,
                                           d_arena, kp, d_ctr);
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
@@ -153,7 +212,7 @@ int main(int argc, char** argv) {
     if (r >= 2) { best = std::min(best, ms); sum += ms; }
   }
   // checksum of the outputs (identical across layout variants up to summation order)
-  std::vector<double> y((size_t)T * 256);
+  std::vector<double> y((size_t)T * 256);  // (T tasks, 256 slots each)
   CK(cudaMemcpy(y.data(), d_arena + y_base, y.size() * 8, cudaMemcpyDeviceToHost));
   double cs = 0;
   for (int t = 0; t < T; ++t)
