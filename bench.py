@@ -343,8 +343,12 @@ def bench_variant(op, args, torch, dev, rank, world, recompute="", e2e=True):
     # per-phase CUDA-event timing on the plan stream (which phase dominates)
     prof = rep.profile_phases(qd, out, iters=max(3, min(args.steps, 10)))
     res = {"rep": rep, "ms": ms, "prof": prof, "clk": clk, "q": q, "out": out}
-    if args.nrhs > 1 and not recompute:
+    if args.nrhs > 1:
         res["multi_rhs"] = bench_multi_rhs(rep, op, torch, dev, k=args.nrhs)
+        if recompute:
+            res["multi_rhs"]["engine"] = ("stored blocks on the DMMA engine, evaluated blocks on "
+                                          "the batched P2P engine (one evaluation per entry for "
+                                          "all right-hand sides)")
     if not e2e:
         return res
     # e2e through the public API with pinned host buffers (out=)

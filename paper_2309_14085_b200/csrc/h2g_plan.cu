@@ -36,6 +36,7 @@
 #include "h2g_kernels.cuh"
 #include "h2g_stream.cuh"
 #include "h2g_p2p.cuh"
+#include "h2g_p2p_batched.cuh"
 
 using namespace h2g;
 
@@ -220,6 +221,14 @@ struct h2g_plan {
     int64_t* d_cta = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    // evaluated terms (plans with kernel-evaluated blocks): the phases' P2P
+    // tasks on the batched kernel-evaluation engine (h2g_p2p_batched.cuh)
+    P2PTask* d_p2p_tasks = nullptr;
+    Term* d_p2p_terms = nullptr;
+    P2PChunk* d_p2p_chunks = nullptr;
+    int* d_ctr = nullptr;                          // 2 task counters per phase
+    std::vector<int64_t> p2p_off;                  // per phase: first P2PTask
+    std::vector<int32_t> p2p_n, p2p_full;          // per phase: tasks, self blocks
     bool ready = false;
     int launches = 0;               // kernels per pass (graph)
   } bat[2];                         // KB = kBatchKB[i]
@@ -1502,6 +1511,10 @@ void free_plan(h2g_plan* p) {
     cudaFree(b.d_recs);
     cudaFree(b.d_cta);
     cudaFree(b.d_red);
+    cudaFree(b.d_p2p_tasks);
+    cudaFree(b.d_p2p_terms);
+    cudaFree(b.d_p2p_chunks);
+    cudaFree(b.d_ctr);
   }
   cudaFree(p->d_hq);
   cudaFree(p->d_hphi);
@@ -1643,7 +1656,11 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
     p->kp.self_value = (d->has_diag ? d->diag : d->zero_value) + d->shift;
     p->kp.gauss_c = d->sigma > 0 ? -1.0 / (2.0 * d->sigma * d->sigma) : 0.0;
     p->kp.check = has_coincident_points(d) ? 1 : 0;
-    p->use_batched = false;  // the tensor-pipe engine streams stored blocks only
+    // nrhs > 1: evaluated tasks run on the batched kernel-evaluation engine
+    // (h2g_p2p_batched.cuh) beside the tensor-pipe engine; H2G_BATCHED_EVAL=0
+    // applies the columns one by one instead
+    const char* be = getenv("H2G_BATCHED_EVAL");
+    if (be && atoi(be) == 0) p->use_batched = false;
   }
   if (nranks > 1) p->use_batched = false;  // leaf tasks of sharded plans add a per-RHS partial
   std::vector<double> local_blob;
@@ -1867,6 +1884,40 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
 // per slot (h2g_kernels.cuh)
 inline int64_t batch_plane(const h2g_plan* p) { return (p->n_slots + 8) * 8; }
 
+// One phase of a batched pass: its split-K reduce tasks, its stored-block
+// tasks on the tensor-pipe engine, its evaluated tasks on the batched P2P
+// engine (disjoint outputs).
+int launch_batched_phase(h2g_plan* p, const h2g_plan::Batched& b, size_t k, int kb,
+                         cudaStream_t s) {
+  const Phase& ph = b.phases[k];
+  const auto& rr = b.red[k];
+  const int64_t ps = batch_plane(p);
+  if (rr.second > 0) {
+    const int grid = std::min<int>(rr.second, 148 * 4);
+    if (kb == 8)
+      reduce_partials_kernel<8><<<grid, 256, 0, s>>>(b.d_red + rr.first, rr.second, b.d_arena, ps);
+    else
+      reduce_partials_kernel<16><<<grid, 256, 0, s>>>(b.d_red + rr.first, rr.second, b.d_arena, ps);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (ph.task_end > ph.task_begin) {
+    if (kb == 8)
+      stream_mma_kernel<8><<<ph.n_cta, kMmaThreads, kMmaSmem, s>>>(
+          b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps, ph.group);
+    else
+      stream_mma_kernel<16><<<ph.n_cta, kMmaThreads, kMmaSmem, s>>>(
+          b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps, ph.group);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (b.p2p_n[k] > 0)
+    CUDA_TRY(p2p_batched_launch(p->kernel_type, p->dim, b.p2p_full[k] || p->kp.check, kb, p->n_sm,
+                                s, b.d_p2p_tasks + b.p2p_off[k], b.p2p_n[k], b.d_p2p_terms,
+                                b.d_p2p_chunks, (const double4*)p->d_recs4,
+                                (const double*)p->d_blob, b.d_arena, ps, p->kp,
+                                b.d_ctr + 2 * k));
+  return H2G_OK;
+}
+
 // Batched-RHS schedule (KB = kBatchKB[which]): the same tasks, cut into
 // chunks whose X (ncols x KB) also fits the ring, over an arena of KB-wide
 // slots; every chunk shared by the consumer warps of the tensor-pipe engine.
@@ -1879,28 +1930,66 @@ int ensure_batched(h2g_plan* p, int which) {
   // ahead of their phase's GEMM launch (no task of a phase reads another's y).
   const HostSchedule& s0 = p->sched;
   HostSchedule sb;
+  HostSchedule sp;          // the phases' P2P tasks (kernel-evaluated terms)
+  std::vector<Phase> pph;   // ... as phases of their own (all on the P2P engine)
   std::vector<RedTask> reds;
+  auto copy_task = [&](HostSchedule& dst, const Task& t) {
+    Task u = t;
+    u.t_begin = (int32_t)dst.terms.size();
+    for (int32_t k = t.t_begin; k < t.t_end; ++k) dst.terms.push_back(s0.terms[k]);
+    u.t_end = (int32_t)dst.terms.size();
+    dst.tasks.push_back(u);
+  };
   for (const Phase& ph : s0.phases) {
     Phase q = ph;
     q.task_begin = (int64_t)sb.tasks.size();
     const int64_t r0 = (int64_t)reds.size();
-    for (int64_t i = ph.task_begin; i < ph.task_end; ++i) {
+    const int64_t se = stream_end_of(ph);
+    for (int64_t i = ph.task_begin; i < se; ++i) {
       const Task& t = s0.tasks[i];
       const Term& t0 = s0.terms[t.t_begin];
       if (t.t_end - t.t_begin == 1 && t0.a_space == 1 && t0.x_off == p->ones_off) {
         reds.push_back(RedTask{t.y_off, t0.a_off, t.m, t0.ncols});
         continue;
       }
-      Task u = t;
-      u.t_begin = (int32_t)sb.terms.size();
-      for (int32_t k = t.t_begin; k < t.t_end; ++k) sb.terms.push_back(s0.terms[k]);
-      u.t_end = (int32_t)sb.terms.size();
-      sb.tasks.push_back(u);
+      copy_task(sb, t);
     }
     q.task_end = (int64_t)sb.tasks.size();
     q.stream_end = -1;
+    q.hybrid = 0;
     b.phases.push_back(q);
     b.red.push_back({r0, (int32_t)((int64_t)reds.size() - r0)});
+    Phase pq = ph;
+    pq.task_begin = pq.stream_end = (int64_t)sp.tasks.size();
+    for (int64_t i = se; i < ph.task_end; ++i) copy_task(sp, s0.tasks[i]);
+    pq.task_end = (int64_t)sp.tasks.size();
+    pq.p2p_full = pq.p2p_sw = 0;
+    pph.push_back(pq);
+  }
+  if (!sp.tasks.empty()) {
+    std::vector<P2PTask> pt;
+    std::vector<Term> pterms;
+    std::vector<P2PChunk> pch;
+    std::vector<P2PStage> pst;
+    build_p2p_lists(sp, pph, pt, pterms, pch, pst, p->d_blob, /*stage=*/false);
+    auto up = [&](void** dptr, const void* src, size_t bytes) -> int {
+      CUDA_TRY(cudaMalloc(dptr, std::max<size_t>(bytes, 16)));
+      if (bytes) CUDA_TRY(cudaMemcpy(*dptr, src, bytes, cudaMemcpyHostToDevice));
+      return H2G_OK;
+    };
+    int r;
+    if ((r = up((void**)&b.d_p2p_tasks, pt.data(), sizeof(P2PTask) * pt.size()))) return r;
+    if ((r = up((void**)&b.d_p2p_terms, pterms.data(), sizeof(Term) * pterms.size()))) return r;
+    if ((r = up((void**)&b.d_p2p_chunks, pch.data(), sizeof(P2PChunk) * pch.size()))) return r;
+    CUDA_TRY(cudaMalloc((void**)&b.d_ctr, sizeof(int) * 2 * pph.size()));
+    CUDA_TRY(cudaMemset(b.d_ctr, 0, sizeof(int) * 2 * pph.size()));
+    p->workspace_bytes += sizeof(P2PTask) * pt.size() + sizeof(Term) * pterms.size() +
+                          sizeof(P2PChunk) * pch.size();
+  }
+  for (const Phase& pq : pph) {
+    b.p2p_off.push_back(pq.p2p_off);
+    b.p2p_n.push_back((int32_t)(pq.task_end - pq.task_begin));
+    b.p2p_full.push_back(pq.p2p_full);
   }
   std::vector<HostChunk> chunks;
   std::vector<int64_t> cta;
@@ -1924,30 +2013,20 @@ int ensure_batched(h2g_plan* p, int which) {
   const int64_t ps = batch_plane(p);
   CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
   for (size_t k = 0; k < b.phases.size(); ++k) {
-    const Phase& ph = b.phases[k];
-    const auto& rr = b.red[k];
-    if (rr.second > 0) {
-      const int grid = std::min<int>(rr.second, 148 * 4);
-      if (kb == 8)
-        reduce_partials_kernel<8><<<grid, 256, 0, p->stream>>>(b.d_red + rr.first, rr.second,
-                                                               b.d_arena, ps);
-      else
-        reduce_partials_kernel<16><<<grid, 256, 0, p->stream>>>(b.d_red + rr.first, rr.second,
-                                                                b.d_arena, ps);
+    int lr = launch_batched_phase(p, b, k, kb, p->stream);
+    if (lr) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(p->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      return lr;
     }
-    if (ph.task_end == ph.task_begin) continue;
-    if (kb == 8)
-      stream_mma_kernel<8><<<ph.n_cta, kMmaThreads, kMmaSmem, p->stream>>>(
-          b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps, ph.group);
-    else
-      stream_mma_kernel<16><<<ph.n_cta, kMmaThreads, kMmaSmem, p->stream>>>(
-          b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps, ph.group);
   }
   CUDA_TRY(cudaStreamEndCapture(p->stream, &b.graph));
   CUDA_TRY(cudaGraphInstantiate(&b.exec, b.graph, 0));
   int launches = 0;
   for (size_t k = 0; k < b.phases.size(); ++k)
-    launches += (b.red[k].second > 0) + (b.phases[k].task_end > b.phases[k].task_begin);
+    launches += (b.red[k].second > 0) + (b.phases[k].task_end > b.phases[k].task_begin) +
+                (b.p2p_n[k] > 0);
   b.launches = launches;
   p->workspace_bytes += sizeof(double) * slots + sizeof(ChunkRec) * recs.size();
   b.ready = true;
@@ -2532,7 +2611,7 @@ int h2g_profile_phases_batched(h2g_plan* p, int kb, int iters, double* ms, int64
                                const char** names, int cap, int* n_out) {
   NvtxRange nvtx_range_("h2g_profile_phases_batched");
   if (!p || iters < 1 || (kb != 8 && kb != 16)) return fail(H2G_ERR_INVALID_ARG, "bad argument");
-  if (p->engine != 1 || p->has_p2p || p->shard.nranks > 1)
+  if (p->engine != 1 || !p->use_batched || p->shard.nranks > 1)
     return fail(H2G_ERR_INVALID_ARG, "batched engine not available for this plan");
   CUDA_TRY(cudaSetDevice(p->device));
   const int which = kb == 8 ? 0 : 1;
@@ -2549,24 +2628,7 @@ int h2g_profile_phases_batched(h2g_plan* p, int kb, int iters, double* ms, int64
   for (int it = 0; it < iters; ++it) {
     CUDA_TRY(cudaEventRecord(ev[0], s));
     for (int k = 0; k < nph; ++k) {
-      const Phase& ph = b.phases[k];
-      const auto& rr = b.red[k];
-      if (rr.second > 0) {
-        const int grid = std::min<int>(rr.second, 148 * 4);
-        if (kb == 8)
-          reduce_partials_kernel<8><<<grid, 256, 0, s>>>(b.d_red + rr.first, rr.second, b.d_arena, ps);
-        else
-          reduce_partials_kernel<16><<<grid, 256, 0, s>>>(b.d_red + rr.first, rr.second, b.d_arena, ps);
-      }
-      if (ph.task_end > ph.task_begin) {
-        if (kb == 8)
-          stream_mma_kernel<8><<<ph.n_cta, kMmaThreads, kMmaSmem, s>>>(b.d_recs, b.d_cta + ph.cta_off,
-                                                                       b.d_arena, ps, ph.group);
-        else
-          stream_mma_kernel<16><<<ph.n_cta, kMmaThreads, kMmaSmem, s>>>(b.d_recs, b.d_cta + ph.cta_off,
-                                                                        b.d_arena, ps, ph.group);
-      }
-      CUDA_TRY(cudaGetLastError());
+      if ((rc = launch_batched_phase(p, b, (size_t)k, kb, s))) return rc;
       CUDA_TRY(cudaEventRecord(ev[k + 1], s));
     }
     CUDA_TRY(cudaEventSynchronize(ev[nph]));

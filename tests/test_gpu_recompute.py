@@ -102,3 +102,37 @@ def test_at_scale_against_stored(N, d, kernel, eps):
             phi = rep.matvec(q)
             assert np.array_equal(phi, rep.matvec(q))
         assert rel_err(phi, ref) <= TOL
+
+
+@pytest.mark.parametrize("nrhs", [16, 21])
+@pytest.mark.parametrize("name", ["g2d_log_h2plusH", "g2d_cfg1_h2star", "g3d_lap_k3_h2star",
+                                  "g3d_lap_k3_h2plusH", "g3d_gauss_k3_h2star"])
+def test_batched_evaluated_engine(name, nrhs):
+    """nrhs > 1 on plans with evaluated blocks: every kernel entry is evaluated
+    once for all right-hand sides (csrc/h2g_p2p_batched.cuh) beside the
+    tensor-pipe engine's stored blocks; equals the reference's matvec column
+    by column (engine.py:250-269 applied to each column), bitwise repeatable,
+    and the column loop (H2G_BATCHED_EVAL=0) to rounding."""
+    import os
+    from paper_2309_14085_b200.gpu_rep import GpuHierRep
+    op, z, meta = load_golden(name)
+    reps = (nrhs + z["Q"].shape[1] - 1) // z["Q"].shape[1]
+    Q = np.ascontiguousarray(np.tile(z["Q"], (1, reps))[:, :nrhs])
+    Q[:, 1::2] *= -0.5  # distinct columns
+    ref = np.tile(z["Phi_ref"], (1, reps))[:, :nrhs].copy()
+    ref[:, 1::2] *= -0.5
+    for mode, share, ev in (("m2l", 1.0, op), ("near,m2l", 0.6, op),
+                            ("", 1.0, op.without_blocks(near=True, m2l=True))):
+        with GpuHierRep(ev, recompute=mode, m2l_share=share) as rep:
+            assert rep.launches_per_matvec(nrhs) < nrhs * rep.launches_per_matvec() // 2
+            P = rep.matmat(Q)
+            assert np.array_equal(P, rep.matmat(Q))
+        for j in range(nrhs):
+            assert rel_err(P[:, j], ref[:, j]) <= TOL, (mode, j)
+    os.environ["H2G_BATCHED_EVAL"] = "0"
+    try:
+        with GpuHierRep(op, recompute="near,m2l") as rep:
+            P0 = rep.matmat(Q)
+    finally:
+        os.environ.pop("H2G_BATCHED_EVAL")
+    assert rel_err(P, P0) <= TOL

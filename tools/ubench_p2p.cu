@@ -17,7 +17,11 @@
 
 #include <cuda_runtime.h>
 
-#ifdef UB_OLD
+#if defined(UB_R01)
+#include "h2g_stream.cuh"
+#include "h2g_p2p_r01.cuh"   // round-1 kernel (no stages): evaluation-only comparisons
+namespace h2g { struct P2PStage { uint64_t src; int64_t x_off; uint32_t bytes; int16_t ncols, shift; }; }
+#elif defined(UB_OLD)
 #include "h2g_p2p_old.cuh"
 #else
 #include "../paper_2309_14085_b200/csrc/h2g_p2p.cuh"
@@ -55,6 +59,8 @@ int main(int argc, char** argv) {
     T = 32768; m_lo = 15; m_hi = 53; nb = 100; c_lo = 15; c_hi = 53; nb2 = 6; l2l = 100;
   } else if (!strcmp(level, "l4r")) {
     T = 4096; m_lo = 71; m_hi = 116; nb = 78; c_lo = 71; c_hi = 116; nb2 = 5; l2l = 100;
+  } else if (!strcmp(level, "l5c")) {  // config 5's leaf level: leaves of ~64 points
+    T = 32768; m_lo = 48; m_hi = 64; nb = 119; c_lo = 48; c_hi = 64;
   } else {  // l5x: exact 32 x 32 blocks
     T = 32768; m_lo = 32; m_hi = 32; nb = 119; c_lo = 32; c_hi = 32;
   }
@@ -120,7 +126,9 @@ int main(int argc, char** argv) {
     q.y_off = y_base + (int64_t)oi * 256;
     q.row_rec = (int32_t)(rng() % (uint64_t)(n_rec / 2 - 256));  // rows: first half of the records
     q.k_begin = (int32_t)chunks.size();
+#ifndef UB_R01
     q.s_begin = (int32_t)stages.size();
+#endif
     for (const Blk& k : protos[t].second) {
       const int nc = k.nc;
       const int64_t x_off = k.x_off;
@@ -128,7 +136,10 @@ int main(int argc, char** argv) {
       if (k.stored) {
         n_stream += e;
         if (boff + (size_t)q.m * nc + 2 > blob_doubles) boff = 0;
-#ifdef UB_OLD
+#if defined(UB_R01)
+        fprintf(stderr, "the round-1 kernel has no stages: share must be 1\n");
+        return 1;
+#elif defined(UB_OLD)
         const int64_t cc = std::max<int64_t>(1, (kP2PStageBytes - 16) / (8 * (int64_t)q.m));
         for (int64_t c0 = 0; c0 < nc; c0 += cc) {
           const int64_t n1 = std::min<int64_t>(cc, nc - c0);
@@ -156,7 +167,9 @@ int main(int argc, char** argv) {
       }
     }
     q.k_end = (int32_t)chunks.size();
+#ifndef UB_R01
     q.s_end = (int32_t)stages.size();
+#endif
     tasks.push_back(q);
   }
   T = n_tasks;
@@ -180,7 +193,11 @@ int main(int argc, char** argv) {
   fill<<<148 * 8, 256>>>(d_arena, n_arena, 1.0);
   CK(cudaDeviceSynchronize());
   P2PKernel kp{};
-#ifdef UB_OLD
+#if defined(UB_R01)
+  auto kfn = p2p_tasks_kernel<1, 3>;
+  const size_t smem = 0;
+  const int threads = kP2PThreads, per_sm = kP2PCtasPerSm;
+#elif defined(UB_OLD)
   auto kfn = p2p_tasks_kernel<1, 3, false>;
   const size_t smem = kP2PSmem;
   const int threads = kP2PThreads, per_sm = kP2PCtasPerSm;
@@ -202,8 +219,12 @@ int main(int argc, char** argv) {
   float best = 1e30f, sum = 0;
   for (int r = 0; r < reps + 2; ++r) {
     CK(cudaEventRecord(e0));
+#if defined(UB_R01)
+    kfn<<<grid, threads, smem>>>(d_tasks, T, d_terms, d_chunks, d_recs, d_blob, d_arena, kp, d_ctr);
+#else
     kfn<<<grid, threads, smem>>>(d_tasks, T, d_terms, d_chunks, d_stages, d_recs, d_blob,
                                           d_arena, kp, d_ctr);
+#endif
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
