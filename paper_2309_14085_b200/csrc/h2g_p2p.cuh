@@ -89,6 +89,9 @@ constexpr int kP2PStageCols = 64;                         // columns of one stag
 constexpr int kP2PSlotX = 8 * (kP2PStageCols + 2);
 constexpr int kP2PSlotBytes = kP2PSlotX + kP2PStageBytes + 16;
 constexpr int kP2PSlots = H2G_P2P_SLOTS;                  // stages in flight per CTA
+// a phase gets streaming warps only if at least this share of its entries is
+// stored (measured: cfg 5's all-evaluated phases lose 12 % with them)
+constexpr double kP2PMinStagedShare = 0.15;
 static_assert(kP2PSlots <= 32, "slot parity bits; first fill by one lane per slot");
 // dynamic smem: [stage slots] + the evaluation warps' chunk buffers + the
 // cross-warp reduction rows + [slot mbarriers, infos] + the task index

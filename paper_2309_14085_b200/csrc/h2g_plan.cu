@@ -569,14 +569,27 @@ void build_p2p_lists(const HostSchedule& s, std::vector<Phase>& phases,
   for (Phase& ph : phases) {
     ph.p2p_off = (int64_t)pt.size();
     // phases with self blocks (the near field) run the FULL kernels, which
-    // have no streaming warp: their stored terms are read directly
+    // have no streaming warp: their stored terms are read directly.  Staging
+    // pays (a streaming warp replaces one of four evaluation warps) only
+    // where a real share of the phase's entries is stored: all-evaluated
+    // operators (config 5's mode) keep their small L2L terms as direct loads.
     bool stage_ph = stage && d_blob;
+    double e_stored = 0.0, e_eval = 0.0;
     for (int64_t i = stream_end_of(ph); stage_ph && i < ph.task_end; ++i)
-      for (int32_t k = s.tasks[i].t_begin; k < s.tasks[i].t_end; ++k)
-        if (s.terms[k].a_space == kRecompute && s.terms[k].pad) {
-          stage_ph = false;
-          break;
+      for (int32_t k = s.tasks[i].t_begin; k < s.tasks[i].t_end; ++k) {
+        const Term& tm = s.terms[k];
+        const double e = (double)s.tasks[i].m * tm.ncols;
+        if (tm.a_space == kRecompute) {
+          e_eval += e;
+          if (tm.pad) {
+            stage_ph = false;
+            break;
+          }
+        } else if (tm.a_space == 0 && tm.lda == s.tasks[i].m) {
+          e_stored += e;
         }
+      }
+    if (e_stored < kP2PMinStagedShare * (e_stored + e_eval)) stage_ph = false;
     for (int64_t i = stream_end_of(ph); i < ph.task_end; ++i) {
       const Task& t = s.tasks[i];
       P2PTask q{};

@@ -13,10 +13,11 @@ from golden_io import golden_names, load_golden, rel_err
 pytestmark = pytest.mark.gpu
 
 
-def _virtual_ranks(op, q, R, recompute=""):
+def _virtual_ranks(op, q, R, recompute="", m2l_share=1.0):
     import torch
     from paper_2309_14085_b200.sharded import ShardedGpuHierRep
-    reps = [ShardedGpuHierRep(op, r, R, device=0, recompute=recompute) for r in range(R)]
+    reps = [ShardedGpuHierRep(op, r, R, device=0, recompute=recompute, m2l_share=m2l_share)
+            for r in range(R)]
     qd = torch.from_numpy(np.asarray(q, dtype=np.float64)).cuda()
     stream = torch.cuda.current_stream().cuda_stream
     mx = max(1, reps[0].info["max_send_slots"])
@@ -109,6 +110,15 @@ def test_virtual_ranks_evaluated_blocks(name, R):
 def test_virtual_ranks_recompute_mask(recompute):
     op, z, meta = load_golden("g3d_lap_h2plusH")
     phi, infos = _virtual_ranks(op, z["q"], 4, recompute=recompute)
+    assert rel_err(phi, z["phi_ref"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["g3d_lap_k3_h2star", "g3d_lap_k3_h2plusH"])
+def test_virtual_ranks_staged_share(name):
+    """The bench's multi-GPU mode: every rank evaluates a share of its M2L
+    entries and stages the rest through its P2P CTAs' streaming warps."""
+    op, z, meta = load_golden(name)
+    phi, infos = _virtual_ranks(op, z["q"], 4, recompute="m2l", m2l_share=0.6)
     assert rel_err(phi, z["phi_ref"]) <= 1e-12
 
 
