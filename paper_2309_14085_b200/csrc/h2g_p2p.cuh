@@ -69,8 +69,11 @@ constexpr int kSelfBit = 1 << 16;
 #ifndef H2G_P2P_STAGE_BYTES
 #define H2G_P2P_STAGE_BYTES 8192
 #endif
+#ifndef H2G_P2P_ASYNC
+#define H2G_P2P_ASYNC 1
+#endif
 #ifndef H2G_P2P_SLOTS
-#define H2G_P2P_SLOTS 4
+#define H2G_P2P_SLOTS (H2G_P2P_ASYNC ? 3 : 4)
 #endif
 #ifndef H2G_P2P_UNROLL
 #define H2G_P2P_UNROLL 2
@@ -95,10 +98,14 @@ constexpr double kP2PMinStagedShare = 0.15;
 static_assert(kP2PSlots <= 32, "slot parity bits; first fill by one lane per slot");
 // dynamic smem: [stage slots] + the evaluation warps' chunk buffers + the
 // cross-warp reduction rows + [slot mbarriers, infos] + the task index
+// kP2PAsync: the warps of a CTA run up to one task apart (two sets of
+// reduction rows; the last warp to finish a task adds them up and fetches the
+// set's next task), so nobody idles at a task-end barrier
+constexpr bool kP2PAsync = H2G_P2P_ASYNC != 0;
 constexpr size_t p2p_smem_bytes(bool sw) {
   return (sw ? (size_t)kP2PSlots * kP2PSlotBytes + (size_t)kP2PSlots * 16 : 0) +
          (size_t)(sw ? kP2PWarpsSW : kP2PWarps) * 2 * kP2PChunk * (sizeof(double) * 4 + 8) +
-         (size_t)(sw ? kP2PWarpsSW + 1 : kP2PWarps) * kMaxRows * 8 + 16;
+         (size_t)(kP2PAsync ? 2 : 1) * (sw ? kP2PWarpsSW + 1 : kP2PWarps) * kMaxRows * 8 + 48;
 }
 static_assert(kP2PCtasSW * (p2p_smem_bytes(true) + 1024) <= 228 * 1024, "P2P smem per SM");
 static_assert(kP2PCtasPerSm * (p2p_smem_bytes(false) + 1024) <= 228 * 1024, "P2P smem per SM");
@@ -478,28 +485,32 @@ p2p_tasks_kernel(const P2PTask* __restrict__ tasks, int n_tasks, const Term* __r
       slots + (SW ? (size_t)kP2PSlots * kP2PSlotBytes : 0));
   auto sx = reinterpret_cast<double (*)[2][kP2PChunk]>(srec + W);
   double* red = reinterpret_cast<double*>(sx + W);
-  uint64_t* sbar = reinterpret_cast<uint64_t*>(red + NW * kMaxRows);
+  constexpr int NSET = kP2PAsync ? 2 : 1;  // sets of reduction rows
+  uint64_t* sbar = reinterpret_cast<uint64_t*>(red + NSET * NW * kMaxRows);
   int* sinfo = reinterpret_cast<int*>(sbar + (SW ? kP2PSlots : 0));
-  int* s_task = sinfo + (SW ? 2 * kP2PSlots : 0);
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(sinfo + (SW ? 2 * kP2PSlots : 0));  // [2]
+  int* s_task = reinterpret_cast<int*>(tbar + 2);                                  // [2]
+  int* s_cnt = s_task + 2;                                                         // [2]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (SW && threadIdx.x == 0) {
-    for (int i = 0; i < kP2PSlots; ++i) mbar_init(&sbar[i], 1);
+  if (threadIdx.x == 0) {
+    if (SW)
+      for (int i = 0; i < kP2PSlots; ++i) mbar_init(&sbar[i], 1);
+    mbar_init(&tbar[0], 1);
+    mbar_init(&tbar[1], 1);
+    s_cnt[0] = s_cnt[1] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();
   uint32_t sphase = 0;  // parity of every slot's barrier (streaming warp)
   griddep_launch_dependents();
   griddep_wait();  // x (and the counters' reset) come from earlier phases
-  for (;;) {
-    if (threadIdx.x == 0) *s_task = atomicAdd(ctr, 1);
-    __syncthreads();
-    const int t = *s_task;
-    if (t >= n_tasks) break;
-    const P2PTask tk = tasks[t];
+  // this warp's share of task tk into the reduction rows at `rd`
+  auto run_task = [&](const P2PTask& tk, double* rd) {
     if (!SW || warp < W)
-      p2p_dispatch<KT, DIM, FULL, W, SW ? kP2PUnrollSW : kP2PUnroll>(tk, terms, chunks, recs, blob, arena, kp, srec[warp], sx[warp],
-                                  red, lane, warp);
+      p2p_dispatch<KT, DIM, FULL, W, SW ? kP2PUnrollSW : kP2PUnroll>(
+          tk, terms, chunks, recs, blob, arena, kp, srec[warp], sx[warp], rd, lane, warp);
     else {  // streaming warp: rows lane + 32 jj, jj < ceil(m / 32)
-      double* myred = red + W * kMaxRows;
+      double* myred = rd + W * kMaxRows;
       const int js = (tk.m + 31) >> 5;
       if (js == 1)
         p2p_stream_task<1>(tk, stages, arena, slots, sbar, sinfo, sphase, myred, lane);
@@ -510,15 +521,69 @@ p2p_tasks_kernel(const P2PTask* __restrict__ tasks, int n_tasks, const Term* __r
       else
         p2p_stream_task<8>(tk, stages, arena, slots, sbar, sinfo, sphase, myred, lane);
     }
-    __syncthreads();
-    double* y = arena + tk.y_off;
-    for (int r = threadIdx.x; r < tk.m; r += 32 * NW) {
-      double sum = red[r];
+  };
+  if constexpr (kP2PAsync) {
+    // Task n of the CTA lives in set n % 2.  A warp finishing its share of a
+    // task counts itself in; the last one adds the warps' rows up in warp
+    // order, stores y, fetches the set's next task and opens it (mbarrier):
+    // warps run up to one task apart, the summation order stays fixed.
+    if (threadIdx.x == 0)
+      for (int b = 0; b < 2; ++b) {
+        s_task[b] = atomicAdd(ctr, 1);
+        mbar_arrive(&tbar[b]);
+      }
+    for (int n = 0;; ++n) {
+      const int b = n & 1;
+      mbar_wait(&tbar[b], (uint32_t)(n >> 1) & 1u);
+      const int t = *reinterpret_cast<volatile int*>(&s_task[b]);
+      if (t >= n_tasks) break;
+      const P2PTask tk = tasks[t];
+      double* rd = red + b * NW * kMaxRows;
+      run_task(tk, rd);
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&s_cnt[b], 1) == NW - 1;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence_block();
+        double* y = arena + tk.y_off;
+        for (int r = lane; r < tk.m; r += 32) {
+          double sum = rd[r];
 #pragma unroll
-      for (int w = 1; w < NW; ++w) sum += red[w * kMaxRows + r];
-      y[r] = sum;
+          for (int w = 1; w < NW; ++w) sum += rd[w * kMaxRows + r];
+          y[r] = sum;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          s_cnt[b] = 0;
+          *reinterpret_cast<volatile int*>(&s_task[b]) = atomicAdd(ctr, 1);
+          __threadfence_block();
+          mbar_arrive(&tbar[b]);
+        }
+      }
     }
-    __syncthreads();  // red / s_task reuse
+    __syncthreads();  // every warp is done before the CTA reports out
+  } else {
+    for (;;) {
+      if (threadIdx.x == 0) s_task[0] = atomicAdd(ctr, 1);
+      __syncthreads();
+      const int t = s_task[0];
+      if (t >= n_tasks) break;
+      const P2PTask tk = tasks[t];
+      run_task(tk, red);
+      __syncthreads();
+      double* y = arena + tk.y_off;
+      for (int r = threadIdx.x; r < tk.m; r += 32 * NW) {
+        double sum = red[r];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) sum += red[w * kMaxRows + r];
+        y[r] = sum;
+      }
+      __syncthreads();  // red / s_task reuse
+    }
   }
   if (threadIdx.x == 0) {
     __threadfence();
