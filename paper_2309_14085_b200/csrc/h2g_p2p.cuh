@@ -70,7 +70,7 @@ constexpr int kSelfBit = 1 << 16;
 #define H2G_P2P_STAGE_BYTES 8192
 #endif
 #ifndef H2G_P2P_ASYNC
-#define H2G_P2P_ASYNC 1
+#define H2G_P2P_ASYNC 0  // measured slower (cfg 3: 10.23 vs 9.95 ms), kept for the record
 #endif
 #ifndef H2G_P2P_SLOTS
 #define H2G_P2P_SLOTS (H2G_P2P_ASYNC ? 3 : 4)
@@ -98,9 +98,12 @@ constexpr double kP2PMinStagedShare = 0.15;
 static_assert(kP2PSlots <= 32, "slot parity bits; first fill by one lane per slot");
 // dynamic smem: [stage slots] + the evaluation warps' chunk buffers + the
 // cross-warp reduction rows + [slot mbarriers, infos] + the task index
-// kP2PAsync: the warps of a CTA run up to one task apart (two sets of
+// kP2PAsync (off): the warps of a CTA run up to one task apart (two sets of
 // reduction rows; the last warp to finish a task adds them up and fetches the
-// set's next task), so nobody idles at a task-end barrier
+// set's next task) instead of meeting at a task-end barrier.  Measured: the
+// M2L phases gain 2 % with streaming warps, but warps spinning on the set's
+// mbarrier take issue slots from the fp64-bound ones (all-evaluated phases
+// lose 4 %) and two reserved tasks per CTA lengthen the phase tails.
 constexpr bool kP2PAsync = H2G_P2P_ASYNC != 0;
 constexpr size_t p2p_smem_bytes(bool sw) {
   return (sw ? (size_t)kP2PSlots * kP2PSlotBytes + (size_t)kP2PSlots * 16 : 0) +
