@@ -179,6 +179,28 @@ def build_op(cfg, variant, n_threads=0, store=None):
     return op, time.perf_counter() - t0
 
 
+def build_op_shared(cfg, variant, rank, world, barrier, tmp_root="/tmp"):
+    """N > 1: ONE native build for the node instead of one per rank.  Rank 0
+    runs the NCA pivot search with every host thread and exports the operator
+    without its raw kernel blocks (store="": transfer operators, pivots,
+    points; ~1 GB); after the barrier every rank loads the export.  Configs
+    that store their blocks re-evaluate them natively (builder.
+    materialize_blocks: bitwise the blocks of a stored build, seconds) -- the
+    caller does that one rank at a time so the node never holds more than one
+    full operator in host memory beside the plans' uploads."""
+    import shutil
+    from paper_2309_14085_b200.packed import PackedOperator
+    path = os.path.join(tmp_root, f"h2g_bench_{cfg['N']}_{cfg['kernel']}_{variant}")
+    tb = 0.0
+    if rank == 0:
+        shutil.rmtree(path, ignore_errors=True)
+        op0, tb = build_op(cfg, variant, n_threads=os.cpu_count() or 1, store="")
+        op0.save_dir(path)
+        del op0
+    barrier()
+    return PackedOperator.load_dir(path), tb
+
+
 def config_dict(cfg, variant, N, kappa, mem_scalars, world):
     """The workload (identical in both arms)."""
     return {"workload": cfg["desc"], "variant": variant, "N": int(N), "kappa": int(kappa),
@@ -373,11 +395,16 @@ def bench_variant(op, args, torch, dev, rank, world, recompute="", e2e=True):
     return res
 
 
-def bench_variant_sharded(op, args, torch, dev, rank, world, recompute=""):
-    """Strong scaling: the operator split over `world` GPUs, one all-gather."""
+def bench_setup_sharded(op, args, dev, rank, world, recompute=""):
+    """This rank's sharded plan (uploads only the blocks its tasks read)."""
     from paper_2309_14085_b200.sharded import ShardedGpuHierRep
-    rep = ShardedGpuHierRep(op, rank, world, device=dev, recompute=recompute,
-                            m2l_share=args.m2l_share)
+    return ShardedGpuHierRep(op, rank, world, device=dev, recompute=recompute,
+                             m2l_share=args.m2l_share)
+
+
+def bench_variant_sharded(rep, op, args, torch, dev, rank, world):
+    """Strong scaling: the operator split over `world` GPUs, one all-gather
+    overlapped with the owned near field."""
     N = op.N
     q = np.random.default_rng(43).standard_normal(N)
     qd = torch.from_numpy(q).to(f"cuda:{dev}")
@@ -476,17 +503,29 @@ def main():
 
     import torch
     if world > 1:
-        torch.distributed.init_process_group("nccl")
+        import datetime
+        # rank 0 builds the operator for the node while the others wait
+        torch.distributed.init_process_group("nccl", timeout=datetime.timedelta(hours=2))
     dev = local if torch.cuda.device_count() > local else 0
     torch.cuda.set_device(dev)
 
     results = {}
     for v in variants:
-        op, tb = build_op(cfg, v, n_threads=n_threads)
-        rc = recompute_for(cfg, args.recompute, op)
         if world > 1:
-            r = bench_variant_sharded(op, args, torch, dev, rank, world, recompute=rc)
+            from paper_2309_14085_b200.builder import materialize_blocks
+            op, tb = build_op_shared(cfg, v, rank, world, torch.distributed.barrier)
+            rc = recompute_for(cfg, args.recompute, op)
+            r = None
+            for turn in range(world):  # one full operator in host memory at a time
+                if turn == rank:
+                    full = op if cfg.get("store") == "" else materialize_blocks(op)
+                    r = bench_setup_sharded(full, args, dev, rank, world, recompute=rc)
+                    del full
+                torch.distributed.barrier()
+            r = bench_variant_sharded(r, op, args, torch, dev, rank, world)
         else:
+            op, tb = build_op(cfg, v, n_threads=n_threads)
+            rc = recompute_for(cfg, args.recompute, op)
             r = bench_variant(op, args, torch, dev, rank, world, recompute=rc)
         r["op"], r["build_s"], r["rc"] = op, tb, rc
         if v == variants[0] and rc and world == 1 and args.streamed_variant and cfg.get("store") != "":

@@ -92,3 +92,25 @@ def test_reference_arm_maps_no_repo_library(tmp_path, bench):
     out = subprocess.run([sys.executable, "-c", code], check=True, capture_output=True, text=True)
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["v"] > 0 and res["so"] is False
+
+
+def test_shared_build_for_multi_gpu_runs(tmp_path):
+    """bench.py N > 1: rank 0 builds once (store=""), every rank loads the
+    export and re-evaluates its raw kernel blocks natively -- bitwise the
+    operator a stored build holds (reference engine.py:176-179, 309-318)."""
+    import numpy as np
+    import bench
+    from paper_2309_14085_b200.builder import materialize_blocks
+    cfg = dict(N=3000, d=3, kernel="lap3d", n_max=32, eps=1e-6, desc="small")
+    calls = []
+    op, tb = bench.build_op_shared(cfg, "h2star-bt", 0, 1, lambda: calls.append(1),
+                                   tmp_root=str(tmp_path))
+    assert calls == [1] and tb > 0
+    full = materialize_blocks(op)
+    ref, _ = bench.build_op(cfg, "h2star-bt")
+    assert full.mem_scalars == ref.mem_scalars == op.mem_scalars
+    # same blocks; the two blobs order and pad them differently
+    from oracle.packed_matvec import packed_matvec
+    q = np.random.default_rng(5).standard_normal(cfg["N"])
+    assert np.array_equal(packed_matvec(full, q), packed_matvec(ref, q))
+    assert bench.recompute_for(cfg, "auto", op) in ("m2l", "near,m2l")
