@@ -76,13 +76,14 @@ constexpr int kSelfBit = 1 << 16;
 #define H2G_P2P_SLOTS (H2G_P2P_ASYNC ? 3 : 4)
 #endif
 #ifndef H2G_P2P_UNROLL
-#define H2G_P2P_UNROLL 2
+#define H2G_P2P_UNROLL 1
 #endif
 #ifndef H2G_P2P_UNROLL_SW
 #define H2G_P2P_UNROLL_SW 1
 #endif
-// columns in flight per lane group in the evaluation loop (measured on cfg 3:
-// beside a streaming warp one column at a time is 2 % faster, alone two are)
+// columns in flight per lane group in the evaluation loop (measured: one
+// column at a time is 2-3 % faster than two, with and without a streaming
+// warp -- the 8 rows per lane already give the chains to overlap)
 constexpr int kP2PUnroll = H2G_P2P_UNROLL;
 constexpr int kP2PUnrollSW = H2G_P2P_UNROLL_SW;
 constexpr int kP2PStageBytes = H2G_P2P_STAGE_BYTES;       // operator data of one stage

@@ -127,6 +127,15 @@ struct HostSchedule {
     int64_t base, m, ncols;
   };
   std::vector<Panelized> panels;
+  // BLR stage-1 factors stacked by source (stack_blr_v): V_k^T (p_k x n_Y,
+  // column-major) of the pairs k sharing the source Y, rows concatenated, in
+  // an extension of the device blob at ext_off (doubles past the export's blob)
+  struct VStack {
+    int64_t ext_off, ny, rows;
+    std::vector<int64_t> v_off, pr;  // per stacked factor: its V in the export, its rank
+  };
+  std::vector<VStack> vstacks;
+  int64_t blob_ext = 0;  // doubles appended to the blob
 };
 
 constexpr int kBlrChunkDoubles = 65536;  // split-K piece of a BLR V^T q product (512 KB)
@@ -411,6 +420,19 @@ void panelize_tall_blocks(HostSchedule& s) {
       u.a_off = base_of[k] + r0 * u.ncols;
       u.lda = t.m;
     }
+}
+
+// Host copy of one stack of BLR V^T factors (HostSchedule::VStack): column c
+// of the stack = the factors' columns c one under the other.
+void vstack_layout(const double* blob, const HostSchedule::VStack& vs, double* out) {
+  int64_t r0 = 0;
+  for (size_t i = 0; i < vs.v_off.size(); ++i) {
+    const double* v = blob + vs.v_off[i];  // p x n_Y column-major (= V row-major)
+    const int64_t pr = vs.pr[i];
+    for (int64_t c = 0; c < vs.ny; ++c)
+      memcpy(out + c * vs.rows + r0, v + c * pr, sizeof(double) * pr);
+    r0 += pr;
+  }
 }
 
 // Host copy of one block in row-panel layout (see panelize_tall_blocks).
@@ -721,6 +743,53 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
       max_parts = std::max<int64_t>(max_parts, (int64_t)pieces[k].size());
     }
   }
+  // ---- BLR V stacking (unsharded, uncompacted plans): the one-piece factors
+  // sharing a source Y become ONE stage-1 task -- their V^T rows concatenated
+  // (re-laid out into an extension of the device blob), one x segment q_Y,
+  // their w slots contiguous -- instead of many 10-20 KB single-chunk tasks
+  // whose per-chunk producer work bounds the phase (cfg 2, (H2+H)*: 48,640
+  // leaf-level tasks at 5.0 TB/s).  blr_vq: w = V^T q_Y, blr.py:83.
+  std::vector<int64_t> stack_of(blr_nnz, -1);
+  const char* vs_env = getenv("H2G_BLR_STACK");
+  if (sh.nranks == 1 && !p->compact && !(vs_env && atoi(vs_env) == 0)) {
+    std::map<int64_t, std::vector<int64_t>> by_src;
+    for (int64_t k = 0; k < blr_nnz; ++k)
+      if (pieces[k].size() == 1 && part_off[k] < 0 && d->blr_rank[k] > 0 &&
+          d->blr_v_off[k] >= 0 && in_blob(d, d->blr_v_off[k], nsz(d->blr_src[k]), d->blr_rank[k]))
+        by_src[d->blr_src[k]].push_back(k);
+    int64_t ext = 0;
+    for (auto& kv : by_src) {
+      const int64_t ny = nsz(kv.first);
+      size_t i = 0;
+      while (i < kv.second.size()) {
+        HostSchedule::VStack vs;
+        vs.ny = ny;
+        vs.rows = 0;
+        size_t j = i;
+        while (j < kv.second.size() && vs.rows + d->blr_rank[kv.second[j]] <= kStreamMaxRows) {
+          vs.rows += d->blr_rank[kv.second[j]];
+          ++j;
+        }
+        if (j - i >= 2) {
+          vs.ext_off = ext;
+          int64_t r0 = 0;
+          for (size_t q = i; q < j; ++q) {
+            const int64_t k = kv.second[q];
+            vs.v_off.push_back(d->blr_v_off[k]);
+            vs.pr.push_back(d->blr_rank[k]);
+            stack_of[k] = (int64_t)s.vstacks.size();
+            w_off[k] = slots + r0;  // contiguous w slots in stacking order
+            r0 += d->blr_rank[k];
+          }
+          slots += vs.rows;
+          ext += (vs.rows * ny + 1) & ~int64_t(1);
+          s.vstacks.push_back(std::move(vs));
+        }
+        i = std::max(j, i + 1);
+      }
+    }
+    s.blob_ext = ext;
+  }
   max_parts = std::max<int64_t>(max_parts, kMaxSplit);
   const int64_t ones_off = slots;  // ones(max_parts): x of the split-K reduce tasks
   slots += max_parts;
@@ -916,11 +985,26 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
     if (pr <= 0) return fail(H2G_ERR_BAD_EXPORT, "BLR factor of rank 0 exported");
     if (!in_blob(d, d->blr_v_off[k], ny, pr) || !in_blob(d, d->blr_u_off[k], nsz(blr_x[k]), pr))
       return fail(H2G_ERR_BAD_EXPORT, "BLR factor out of blob");
+    if (stack_of[k] >= 0) continue;  // part of a stacked task (below)
     for (size_t i = 0; i < pieces[k].size(); ++i) {
       const Piece& pc = pieces[k][i];
       if (pc.owner != sh.rank) continue;
       add_term(s, d->blr_v_off[k] + pc.c0 * pr, p->q_tree + st[y] + pc.c0, pr, pc.c1 - pc.c0);
       emit_task(s, part_off[k] >= 0 ? part_off[k] + (int64_t)i * pr : w_off[k], pr, bytes);
+    }
+  }
+  {
+    const int64_t ext0 = (d->blob_len + 1) & ~int64_t(1);  // the extension starts 16-byte aligned
+    std::vector<int64_t> first_w(s.vstacks.size(), -1), src_of(s.vstacks.size(), -1);
+    for (int64_t k = 0; k < blr_nnz; ++k)
+      if (stack_of[k] >= 0 && first_w[stack_of[k]] < 0) {
+        first_w[stack_of[k]] = w_off[k];
+        src_of[stack_of[k]] = d->blr_src[k];
+      }
+    for (size_t v = 0; v < s.vstacks.size(); ++v) {
+      const HostSchedule::VStack& vs = s.vstacks[v];
+      add_term(s, ext0 + vs.ext_off, p->q_tree + st[src_of[v]], vs.rows, vs.ny);
+      emit_task(s, first_w[v], vs.rows, bytes);
     }
   }
   s.phases.back().alg_bytes = bytes;
@@ -1735,8 +1819,32 @@ int create_impl(const h2g_export_desc* d, int device, h2g_plan** out, int rank =
         return r;
       std::vector<double>().swap(local_blob);
     } else {
-      p->blob_len = d->blob_len;
-      if ((r = upload((void**)&p->d_blob, d->blob, sizeof(double) * d->blob_len))) return r;
+      const int64_t ext0 = (d->blob_len + 1) & ~int64_t(1);
+      p->blob_len = ext0 + s.blob_ext;
+      CUDA_TRY(cudaMalloc((void**)&p->d_blob, sizeof(double) * std::max<int64_t>(p->blob_len, 2)));
+      if (d->blob_len > 0)
+        CUDA_TRY(cudaMemcpy(p->d_blob, d->blob, sizeof(double) * d->blob_len,
+                            cudaMemcpyHostToDevice));
+      {  // stacked BLR V^T factors (stack_blr_v) behind the export's blob, in batches
+        std::vector<double> buf;
+        size_t v0 = 0;
+        while (v0 < s.vstacks.size()) {
+          size_t v1 = v0;
+          int64_t len = 0;
+          while (v1 < s.vstacks.size() && (v1 == v0 || len < (int64_t(1) << 25))) {
+            len = s.vstacks[v1].ext_off - s.vstacks[v0].ext_off +
+                  ((s.vstacks[v1].rows * s.vstacks[v1].ny + 1) & ~int64_t(1));
+            ++v1;
+          }
+          buf.assign((size_t)len, 0.0);
+          for (size_t v = v0; v < v1; ++v)
+            vstack_layout(d->blob, s.vstacks[v],
+                          buf.data() + (s.vstacks[v].ext_off - s.vstacks[v0].ext_off));
+          CUDA_TRY(cudaMemcpy(p->d_blob + ext0 + s.vstacks[v0].ext_off, buf.data(),
+                              sizeof(double) * len, cudaMemcpyHostToDevice));
+          v0 = v1;
+        }
+      }
       std::vector<double> pan;
       for (const auto& b : s.panels) {  // tall blocks -> row panels (panelize_tall_blocks)
         panel_layout(d->blob + b.base, b.m, b.ncols, pan);
@@ -2480,8 +2588,13 @@ int h2g_schedule_build(const h2g_export_desc* desc, int rank, int nranks, h2g_sc
   if (rc) return rc;
   h2g_sched* o = new h2g_sched();
   if (tmp.compact) compact_blob(desc, s, o->blob);
-  if (!s.panels.empty()) {  // the blob the device holds: tall blocks as row panels
-    o->blob.assign(desc->blob, desc->blob + desc->blob_len);
+  if (!s.panels.empty() || !s.vstacks.empty()) {
+    // the blob the device holds: tall blocks as row panels, stacked BLR V^T
+    // factors in an extension behind the export's blob
+    const int64_t ext0 = (desc->blob_len + 1) & ~int64_t(1);
+    o->blob.assign((size_t)(ext0 + s.blob_ext), 0.0);
+    std::copy(desc->blob, desc->blob + desc->blob_len, o->blob.begin());
+    for (const auto& vs : s.vstacks) vstack_layout(desc->blob, vs, o->blob.data() + ext0 + vs.ext_off);
     std::vector<double> pan;
     for (const auto& b : s.panels) {
       panel_layout(desc->blob + b.base, b.m, b.ncols, pan);

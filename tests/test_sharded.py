@@ -120,8 +120,10 @@ def test_tall_blocks_as_row_panels(variant):
     q = np.random.default_rng(43).standard_normal(op.N)
     ref = packed_matvec(op, q)
     view = schedule_view(op, 0, 1)
-    assert len(view["blob"]) == len(op.blob)            # row panels applied
-    assert not np.array_equal(view["blob"], op.blob)
+    # row panels applied in place; (H2+H)*: stacked BLR V^T factors appended
+    assert len(view["blob"]) >= len(op.blob)
+    assert (len(view["blob"]) > len(op.blob) + 1) == (variant == "h2plusH-star")
+    assert not np.array_equal(view["blob"][:len(op.blob)], op.blob)
     assert rel_err(emulate_matvec(op, q, 1), ref) <= 1e-13
     assert rel_err(emulate_matvec(op, q, 2), ref) <= 1e-13
 
@@ -151,3 +153,21 @@ def test_shard_level_follows_north_star():
     op, z, meta = load_golden("g3d_lap_k3_h2star")
     for R in (2, 4, 8):
         assert schedule_view(op, 0, R)["level"] == 3
+
+
+def test_blr_factors_stacked_by_source(monkeypatch):
+    """Unsharded (H2+H)* schedules apply the BLR stage-1 factors V_XY^T that
+    share a source Y as ONE task (rows concatenated in an extension of the
+    blob, one x segment q_Y; w = V^T q_Y, blr.py:83): fewer, larger stage-1
+    tasks, same result as the reference's matvec either way."""
+    op, z, meta = load_golden("g2d_cfg1_h2plusH")
+    stacked = schedule_view(op, 0, 1)
+    phi = emulate_matvec(op, z["q"], 1)
+    monkeypatch.setenv("H2G_BLR_STACK", "0")
+    plain = schedule_view(op, 0, 1)
+    phi0 = emulate_matvec(op, z["q"], 1)
+    n_vq = lambda v: int(v["phases"][1][1] - v["phases"][1][0])   # phase 1 = blr_vq
+    assert n_vq(stacked) < n_vq(plain)
+    assert len(stacked["blob"]) > len(op.blob) and len(plain["blob"]) == 0
+    assert int(stacked["tasks"][stacked["phases"][1][0]:stacked["phases"][1][1], 1].max()) <= 256
+    assert rel_err(phi, z["phi_ref"]) <= 1e-13 and rel_err(phi0, z["phi_ref"]) <= 1e-13
