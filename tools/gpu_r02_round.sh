@@ -15,5 +15,5 @@ timeout 900 python tools/sanitize_cases.py > gpurun_out/sanitize_plain.log 2>&1
 # (compute-sanitizer is closed on this pool: profiles/sanitizer_r02.md)
 if [ "${NCU_CFG3:-0}" = "1" ]; then bash tools/gpu_ncu_cfg3.sh; fi
 # launch list of the bench command (kernel names and durations; cold-cache, serialised)
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --nrhs 1 --cpu-budget 1 --streamed-variant 0 > gpurun_out/launches.log 2>&1
+[ "${LAUNCH_LIST:-1}" = "1" ] && timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --nrhs 1 --cpu-budget 1 --streamed-variant 0 > gpurun_out/launches.log 2>&1
 timeout 1500 python bench.py --config cfg5s --steps 10 --warmup 5 > gpurun_out/bench_cfg5s.json 2> gpurun_out/bench_cfg5s.err; echo "rc $?" >> gpurun_out/bench_cfg5s.err

@@ -1,5 +1,5 @@
 #!/bin/bash
-# P2P engine microbenchmark variants (tools/ubench_p2p.cu, prebuilt under scratch/ub/)
+# P2P engine microbenchmark variants (tools/ubench_p2p.cu, prebuilt under scratch/ub/ by tools/build_ubench_p2p.sh)
 mkdir -p gpurun_out
 out=gpurun_out/ubench_p2p.jsonl
 : > $out

@@ -7,7 +7,10 @@
 // kernel of csrc/h2g_p2p.cuh; compile-time variants through -D macros:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
 //        --expt-relaxed-constexpr -I include -o ubench_p2p tools/ubench_p2p.cu
-//   ./ubench_p2p l5 0.7
+//   ./ubench_p2p l5r 0.6
+// -DUB_OLD / -DUB_R01 build against earlier revisions of the kernel header for
+// comparison (git show <rev>:paper_2309_14085_b200/csrc/h2g_p2p.cuh into
+// scratch/old/h2g_p2p_old.cuh resp. scratch/r01/h2g_p2p_r01.cuh, -I that dir).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
