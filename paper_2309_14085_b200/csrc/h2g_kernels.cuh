@@ -134,15 +134,17 @@ static __global__ void scatter_perm_kernel(const double* __restrict__ in,
 // Batched-RHS arena: KB / 8 planes of 8 doubles per slot; RHS b of slot s at
 // (b >> 3) * ps + 8 s + (b & 7) (h2g_stream.cuh, stream_mma_kernel).
 // batched RHS: q_tree (slot i of the planes at `out`) = q[perm[i] * ld + col0 + b]
+// (thread = one (slot, RHS) pair, RHS fastest: a row of q is read as one
+// contiguous run of KB doubles and lands as contiguous 64-byte plane rows)
 template <int KB>
 __global__ void gather_batch_kernel(const double* __restrict__ q, int64_t ld, int64_t col0,
                                     int nb, const int32_t* __restrict__ perm,
                                     double* __restrict__ out, int64_t n, int64_t ps) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double* src = q + (int64_t)perm[i] * ld + col0;
-#pragma unroll
-    for (int b = 0; b < KB; ++b) out[(b >> 3) * ps + i * 8 + (b & 7)] = b < nb ? src[b] : 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * KB;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / KB;
+    const int b = (int)(t % KB);
+    out[(b >> 3) * ps + i * 8 + (b & 7)] = b < nb ? q[(int64_t)perm[i] * ld + col0 + b] : 0.0;
   }
 }
 
@@ -151,12 +153,11 @@ template <int KB>
 __global__ void scatter_batch_kernel(const double* __restrict__ in,
                                      const int32_t* __restrict__ perm, double* __restrict__ phi,
                                      int64_t ld, int64_t col0, int nb, int64_t n, int64_t ps) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double* dst = phi + (int64_t)perm[i] * ld + col0;
-#pragma unroll
-    for (int b = 0; b < KB; ++b)
-      if (b < nb) dst[b] = in[(b >> 3) * ps + i * 8 + (b & 7)];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * KB;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / KB;
+    const int b = (int)(t % KB);
+    if (b < nb) phi[(int64_t)perm[i] * ld + col0 + b] = in[(b >> 3) * ps + i * 8 + (b & 7)];
   }
 }
 

@@ -164,7 +164,21 @@ struct HostChunk {      // streaming chunk before decoding into a ChunkRec
   int32_t flags;
   int32_t seg_begin;    // segments [seg_begin, seg_begin + n_seg)
   int32_t n_seg;
+  int32_t pad_ldas;     // batched engine: contiguous columns staged one bulk copy per column at
+                        // this smem stride (conflict-free A fragments); 0: one copy, stride m
 };
+
+// Batched (DMMA) engine: smem column stride of a padded chunk.  A fragment
+// lane (row rq = lane / 4, column kq = lane % 4) reads A[kq * ldas + rq]; with
+// ldas = m = 64 the four columns of a k-step share their banks (4-way
+// conflict on every A load).  ldas == 4 (mod 8) spreads a half-warp's 4 x 4
+// elements over all 16 eight-byte bank pairs.  (>= m + 2, even: a column copy
+// starts 16-byte aligned and may carry one leading and one trailing double.)
+inline int mma_pad_ldas(int m) {
+  int e = ((m + 1) & ~1) + 2;
+  while ((e & 7) != 4) e += 2;
+  return e;
+}
 
 struct Seg {
   int64_t x_off;        // arena slot of x for the segment's first column
@@ -1211,6 +1225,10 @@ int build_schedule(const h2g_export_desc* d, h2g_plan* p, HostSchedule& s, const
 void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
                   std::vector<HostChunk>& chunks, std::vector<Seg>& segs,
                   std::vector<int64_t>& cta, int kb = 1, bool mma = false) {
+  // batched engine: tasks at least this tall stage their contiguous chunks
+  // column by column at a padded stride (0: never); H2G_MMA_PAD_MIN_M: tests
+  int pad_min_m = kMmaPad ? kMmaPadMinM : 0;
+  if (const char* e = getenv("H2G_MMA_PAD_MIN_M")) pad_min_m = atoi(e);
   for (Phase& ph : phases) {
     if (ph.kind != PH_GEMV) continue;
     const int64_t nt = stream_end_of(ph) - ph.task_begin;
@@ -1250,7 +1268,8 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
       for (int32_t k = t.t_begin; k < t.t_end; ++k) {
         const Term& tm = s.terms[k];
         const bool strided = tm.lda != t.m;
-        const int64_t ldas = strided ? ((t.m + 1) & ~1) + 2 : t.m;
+        const bool pad = mma && pad_min_m > 0 && !strided && t.m >= pad_min_m;
+        const int64_t ldas = strided ? ((t.m + 1) & ~1) + 2 : (pad ? mma_pad_ldas(t.m) : t.m);
         int64_t per = std::max<int64_t>(
             1, std::min<int64_t>(kChunkCols, mma ? chunk_mma / (ldas + kb)
                                                  : kChunkA / std::max<int64_t>(ldas, 1)));
@@ -1259,6 +1278,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
           const int64_t cap = (kRingMma / 2) / (ldas + kb);
           if (!strided)
             per = std::max<int64_t>(per, std::min<int64_t>({kMmaMinCols, cap, kChunkCols}));
+          if (pad) per = std::min<int64_t>(per, 32);  // one bulk copy per column (producer lane)
           if (per >= 4) per &= ~int64_t(3);
         }
         int64_t c0 = 0;
@@ -1268,6 +1288,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
           const bool x_adjacent =
               open && !segs.empty() && segs.back().x_off + segs.back().ncols == tm.x_off + c0;
           if (open && !strided && a_here == a_end && pc.back().a_space == tm.a_space &&
+              (pc.back().pad_ldas > 0) == pad &&
               (pc.back().n_seg < kMaxSeg || x_adjacent) && pc.back().ncols < per_open) {
             take = std::min<int64_t>(tm.ncols - c0, per_open - pc.back().ncols);
             if (x_adjacent) {  // x continues the previous segment: one copy serves both
@@ -1290,6 +1311,7 @@ void build_chunks(HostSchedule& s, std::vector<Phase>& phases, int n_cta,
             c.flags = 0;
             c.seg_begin = (int32_t)segs.size();
             c.n_seg = 1;
+            c.pad_ldas = pad ? (int32_t)ldas : 0;
             segs.push_back(Seg{tm.x_off + c0, (int32_t)take, 0});
             pc.push_back(c);
             cost += 1024.0;
@@ -1399,7 +1421,7 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
     int64_t strided_ext = 0;
     const uint64_t blob = c.a_space ? arena : blob0;
     if (c.ncols > 0) {
-      const bool strided = c.lda != c.m;
+      const bool strided = c.lda != c.m || c.pad_ldas > 0;
       if (!strided) {
         const int64_t sh = c.a_off & 1;
         r.ldas = c.m;
@@ -1410,7 +1432,7 @@ void make_records(const std::vector<HostChunk>& chunks, const std::vector<Seg>& 
         d.bytes = round16(8 * (sh + (int64_t)c.m * c.ncols));
         total += d.bytes;
       } else {  // strided run: one bulk copy per column, issued by the producer lanes
-        r.ldas = ((c.m + 1) & ~1) + 2;
+        r.ldas = c.pad_ldas > 0 ? c.pad_ldas : ((c.m + 1) & ~1) + 2;
         r.a_shift = (int32_t)(c.a_off & 1);
         r.odd_lda = (c.lda & 1) ? 1 : 0;
         r.flags |= kStridedRun;
@@ -2190,18 +2212,18 @@ int matvec_body(h2g_plan* p, const double* q, double* phi, int64_t n, int64_t nr
       const int nb = (int)std::min<int64_t>(kb, nrhs - c0);
       const int64_t ps = batch_plane(p);
       if (kb == 8)
-        gather_batch_kernel<8><<<grid_for(n), 256, 0, s>>>(
+        gather_batch_kernel<8><<<grid_for(n * 8), 256, 0, s>>>(
             q, ld, c0, nb, p->d_perm, b.d_arena + (size_t)p->q_tree * 8, n, ps);
       else
-        gather_batch_kernel<16><<<grid_for(n), 256, 0, s>>>(
+        gather_batch_kernel<16><<<grid_for(n * 16), 256, 0, s>>>(
             q, ld, c0, nb, p->d_perm, b.d_arena + (size_t)p->q_tree * 8, n, ps);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaGraphLaunch(b.exec, s));
       if (kb == 8)
-        scatter_batch_kernel<8><<<grid_for(n), 256, 0, s>>>(
+        scatter_batch_kernel<8><<<grid_for(n * 8), 256, 0, s>>>(
             b.d_arena + (size_t)p->phi_tree * 8, p->d_perm, phi, ld, c0, nb, n, ps);
       else
-        scatter_batch_kernel<16><<<grid_for(n), 256, 0, s>>>(
+        scatter_batch_kernel<16><<<grid_for(n * 16), 256, 0, s>>>(
             b.d_arena + (size_t)p->phi_tree * 8, p->d_perm, phi, ld, c0, nb, n, ps);
       CUDA_TRY(cudaGetLastError());
       c0 += nb;

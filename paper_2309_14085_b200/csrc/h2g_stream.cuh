@@ -363,6 +363,17 @@ constexpr bool kMmaGroupMode = H2G_MMA_GROUP != 0;  // wide phases in group mode
 #ifndef H2G_MMA_DUAL
 #define H2G_MMA_DUAL 0  // measured: no gain at cfg 2 (1.958 -> 1.973 ms per 16 RHS)
 #endif
+#ifndef H2G_MMA_PAD
+#define H2G_MMA_PAD 0      // contiguous chunks of tall tasks staged column by column, padded stride
+#endif
+#ifndef H2G_MMA_PAD_MIN_M
+#define H2G_MMA_PAD_MIN_M 48
+#endif
+constexpr bool kMmaPad = H2G_MMA_PAD != 0;
+constexpr int kMmaPadMinM = H2G_MMA_PAD_MIN_M;
+#ifndef H2G_MMA_PIPE
+#define H2G_MMA_PIPE 1  // software-pipelined fragment loads in consume_mma (cfg 2 leaf pass 644 -> 628 us)
+#endif
 constexpr bool kMmaDualAcc = H2G_MMA_DUAL != 0;     // two accumulator sets for short row groups
 constexpr int kMmaGroupMin = H2G_MMA_GROUP_MIN;     // smallest group (warps per chunk stream)
 constexpr int kChunkAMmaTall = H2G_MMA_CHUNK_TALL;  // chunk of group-mode phases with tasks
@@ -444,6 +455,33 @@ __device__ __forceinline__ void consume_mma(const double* __restrict__ Ab, int l
       Bp += 2 * adv_b;
     }
   }
+#if H2G_MMA_PIPE
+  // software-pipelined: the fragments of k-step t + 1 are loaded before the
+  // DMMAs of k-step t issue, so the LDS latency hides behind the tensor pipe
+  if (t < n_my) {
+    double a[TPW], b[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) b[nt] = Bp[nt * xps];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) a[i] = Ap[i * tstride];
+#pragma unroll 2
+    for (++t; t < n_my; ++t) {
+      Ap += adv_a;
+      Bp += adv_b;
+      double an[TPW], bn[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) bn[nt] = Bp[nt * xps];
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) an[i] = Ap[i * tstride];
+      mma_step<TPW, NT>(a, b, c);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) b[nt] = bn[nt];
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) a[i] = an[i];
+    }
+    mma_step<TPW, NT>(a, b, c);
+  }
+#else
 #pragma unroll 2
   for (; t < n_my; ++t) {
     double a[TPW], b[NT];
@@ -455,6 +493,7 @@ __device__ __forceinline__ void consume_mma(const double* __restrict__ Ab, int l
     Ap += adv_a;
     Bp += adv_b;
   }
+#endif
   // k tail (ncols % 4 columns): the column group holding k-step `full`
   if ((ncols & 3) && (full % wk) == w_k) {
     const bool ok = 4 * full + kq < ncols;

@@ -146,6 +146,27 @@ def test_batched_group_mode(monkeypatch, name):
         assert np.array_equal(Phi, rep.matmat(Q))  # bitwise repeatable
 
 
+@pytest.mark.parametrize("group", [False, True])
+@pytest.mark.parametrize("name", NAMES)
+def test_batched_padded_chunks(monkeypatch, name, group):
+    """Padded-stride chunks of the batched engine (contiguous columns staged
+    one bulk copy per column so that the A fragments read conflict-free;
+    normally only for tall tasks) forced on every task, in k-split and group
+    mode, incl. odd row counts and odd blob offsets (alternating shifts)."""
+    from paper_2309_14085_b200.gpu_rep import GpuHierRep
+    op, z, meta = load_golden(name)
+    monkeypatch.setenv("H2G_MMA_PAD_MIN_M", "1")
+    if group:
+        monkeypatch.setenv("H2G_MMA_GROUP_MIN_TASKS", "1")
+    with GpuHierRep(op) as rep:
+        Q = np.random.default_rng(13).standard_normal((op.N, 21))
+        Phi = rep.matmat(Q)
+        for j in (0, 7, 15, 16, 20):
+            assert rel_err(Phi[:, j], rep.matvec(Q[:, j])) <= 1e-13
+            assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= TOL
+        assert np.array_equal(Phi, rep.matmat(Q))  # bitwise repeatable
+
+
 def test_batched_engine_edge_widths(reps):
     """2 and 9 right-hand sides (zero-padded passes) and a zero block."""
     rep, op, z, meta = reps[NAMES[0]]
