@@ -25,7 +25,8 @@ NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
 
 TARGETS = {
     "libh2g.so": (["h2g_plan.cu", "h2g_p2p_launch.cu"],
-                  ["h2g_kernels.cuh", "h2g_stream.cuh", "h2g_p2p.cuh", "h2g_eval.cuh"], "h2g.h"),
+                  ["h2g_kernels.cuh", "h2g_stream.cuh", "h2g_p2p.cuh", "h2g_eval.cuh",
+                   "h2g_p2p_batched.cuh", "h2g_mma_direct.cuh"], "h2g.h"),
     "libh2b.so": (["h2b_build.cpp"], [], "h2b.h"),
 }
 CXX = os.environ.get("H2_CXX", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++")

@@ -37,6 +37,7 @@
 #include "h2g_stream.cuh"
 #include "h2g_p2p.cuh"
 #include "h2g_p2p_batched.cuh"
+#include "h2g_mma_direct.cuh"
 
 using namespace h2g;
 
@@ -250,6 +251,14 @@ struct h2g_plan {
     Term* d_p2p_terms = nullptr;
     P2PChunk* d_p2p_chunks = nullptr;
     int* d_ctr = nullptr;                          // 2 task counters per phase
+    // direct-load DMMA engine (h2g_mma_direct.cuh): wide phases' tasks as
+    // (task, row group) items over the batched schedule's task / term lists
+    Task* d_dtasks = nullptr;
+    Term* d_dterms = nullptr;
+    DItem* d_ditems = nullptr;
+    int* d_dctr = nullptr;                         // one item counter per phase
+    std::vector<int64_t> d_off;                    // per phase: first item
+    std::vector<int32_t> d_n;                      // per phase: items (0: ring engine)
     std::vector<int64_t> p2p_off;                  // per phase: first P2PTask
     std::vector<int32_t> p2p_n, p2p_full;          // per phase: tasks, self blocks
     bool ready = false;
@@ -1634,6 +1643,10 @@ void free_plan(h2g_plan* p) {
     cudaFree(b.d_p2p_terms);
     cudaFree(b.d_p2p_chunks);
     cudaFree(b.d_ctr);
+    cudaFree(b.d_dtasks);
+    cudaFree(b.d_dterms);
+    cudaFree(b.d_ditems);
+    cudaFree(b.d_dctr);
   }
   cudaFree(p->d_hq);
   cudaFree(p->d_hphi);
@@ -2043,7 +2056,20 @@ int launch_batched_phase(h2g_plan* p, const h2g_plan::Batched& b, size_t k, int 
       reduce_partials_kernel<16><<<grid, 256, 0, s>>>(b.d_red + rr.first, rr.second, b.d_arena, ps);
     CUDA_TRY(cudaGetLastError());
   }
-  if (ph.task_end > ph.task_begin) {
+  if (ph.task_end > ph.task_begin && b.d_n[k] > 0) {
+    CUDA_TRY(cudaMemsetAsync(b.d_dctr + k, 0, sizeof(int), s));
+    const int grid = (int)std::min<int64_t>((b.d_n[k] + kDirectWarps - 1) / kDirectWarps,
+                                            (int64_t)p->n_sm * kDirectCtasPerSm);
+    if (kb == 8)
+      direct_mma_kernel<8><<<grid, 32 * kDirectWarps, 0, s>>>(
+          b.d_ditems + b.d_off[k], b.d_n[k], b.d_dtasks, b.d_dterms, (const double*)p->d_blob,
+          b.d_arena, ps, b.d_dctr + k);
+    else
+      direct_mma_kernel<16><<<grid, 32 * kDirectWarps, 0, s>>>(
+          b.d_ditems + b.d_off[k], b.d_n[k], b.d_dtasks, b.d_dterms, (const double*)p->d_blob,
+          b.d_arena, ps, b.d_dctr + k);
+    CUDA_TRY(cudaGetLastError());
+  } else if (ph.task_end > ph.task_begin) {
     if (kb == 8)
       stream_mma_kernel<8><<<ph.n_cta, kMmaThreads, kMmaSmem, s>>>(
           b.d_recs, b.d_cta + ph.cta_off, b.d_arena, ps, ph.group);
@@ -2138,6 +2164,56 @@ int ensure_batched(h2g_plan* p, int which) {
   std::vector<int64_t> cta;
   std::vector<Seg> segs;
   build_chunks(sb, b.phases, p->n_sm * kMmaCtasPerSm, chunks, segs, cta, kb, /*mma=*/true);
+  {  // direct-load engine for the wide (group-mode) phases: H2G_MMA_DIRECT=1
+    const char* e = getenv("H2G_MMA_DIRECT");
+    const bool direct = e ? atoi(e) != 0 : kMmaDirectDefault;
+    std::vector<DItem> items;
+    b.d_off.assign(b.phases.size(), 0);
+    b.d_n.assign(b.phases.size(), 0);
+    for (size_t k = 0; direct && k < b.phases.size(); ++k) {
+      const Phase& ph = b.phases[k];
+      if (ph.kind != PH_GEMV || ph.group <= 0) continue;
+      bool blob_only = true;
+      for (int64_t i = ph.task_begin; i < ph.task_end && blob_only; ++i)
+        for (int32_t j = sb.tasks[i].t_begin; j < sb.tasks[i].t_end; ++j)
+          if (sb.terms[j].a_space != 0) blob_only = false;
+      if (!blob_only) continue;
+      b.d_off[k] = (int64_t)items.size();
+      for (int64_t i = ph.task_begin; i < ph.task_end; ++i) {
+        const Task& t = sb.tasks[i];
+        const int rt = (t.m + 7) / 8;
+        if (t.t_end == t.t_begin || rt == 0) {  // no terms: the item writes zeros
+          for (int r0 = 0; r0 < std::max(rt, 1); r0 += kDirectTiles)
+            items.push_back(DItem{(int32_t)i, (int16_t)r0,
+                                  (int16_t)std::min(kDirectTiles, std::max(rt, 1) - r0)});
+          continue;
+        }
+        const int ni = (rt + kDirectTiles - 1) / kDirectTiles;  // row groups, evenly sized
+        int r0 = 0;
+        for (int g = 0; g < ni; ++g) {
+          const int nt = rt / ni + (g < rt % ni ? 1 : 0);
+          items.push_back(DItem{(int32_t)i, (int16_t)r0, (int16_t)nt});
+          r0 += nt;
+        }
+      }
+      b.d_n[k] = (int32_t)((int64_t)items.size() - b.d_off[k]);
+    }
+    if (!items.empty()) {
+      CUDA_TRY(cudaMalloc((void**)&b.d_dtasks, sizeof(Task) * sb.tasks.size()));
+      CUDA_TRY(cudaMemcpy(b.d_dtasks, sb.tasks.data(), sizeof(Task) * sb.tasks.size(),
+                          cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMalloc((void**)&b.d_dterms, sizeof(Term) * std::max<size_t>(1, sb.terms.size())));
+      CUDA_TRY(cudaMemcpy(b.d_dterms, sb.terms.data(), sizeof(Term) * sb.terms.size(),
+                          cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMalloc((void**)&b.d_ditems, sizeof(DItem) * items.size()));
+      CUDA_TRY(cudaMemcpy(b.d_ditems, items.data(), sizeof(DItem) * items.size(),
+                          cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMalloc((void**)&b.d_dctr, sizeof(int) * b.phases.size()));
+      CUDA_TRY(cudaMemset(b.d_dctr, 0, sizeof(int) * b.phases.size()));
+      p->workspace_bytes += sizeof(Task) * sb.tasks.size() + sizeof(Term) * sb.terms.size() +
+                            sizeof(DItem) * items.size();
+    }
+  }
   const size_t slots = (size_t)(p->n_slots + 8) * kb;
   CUDA_TRY(cudaMalloc((void**)&b.d_arena, sizeof(double) * slots));
   CUDA_TRY(cudaMemset(b.d_arena, 0, sizeof(double) * slots));

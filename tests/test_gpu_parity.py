@@ -167,6 +167,24 @@ def test_batched_padded_chunks(monkeypatch, name, group):
         assert np.array_equal(Phi, rep.matmat(Q))  # bitwise repeatable
 
 
+@pytest.mark.parametrize("name", NAMES)
+def test_batched_direct_load_engine(monkeypatch, name):
+    """Experimental direct-load DMMA engine (h2g_mma_direct.cuh: A fragments
+    straight from global memory, (task, row group) work items) selected for
+    every phase: 16 + 5 RHS equal the single-RHS matvec and the oracle."""
+    from paper_2309_14085_b200.gpu_rep import GpuHierRep
+    op, z, meta = load_golden(name)
+    monkeypatch.setenv("H2G_MMA_DIRECT", "1")
+    monkeypatch.setenv("H2G_MMA_GROUP_MIN_TASKS", "1")
+    with GpuHierRep(op) as rep:
+        Q = np.random.default_rng(14).standard_normal((op.N, 21))
+        Phi = rep.matmat(Q)
+        for j in (0, 7, 15, 16, 20):
+            assert rel_err(Phi[:, j], rep.matvec(Q[:, j])) <= 1e-13
+            assert rel_err(Phi[:, j], packed_matvec(op, Q[:, j])) <= TOL
+        assert np.array_equal(Phi, rep.matmat(Q))  # bitwise repeatable
+
+
 def test_batched_engine_edge_widths(reps):
     """2 and 9 right-hand sides (zero-padded passes) and a zero block."""
     rep, op, z, meta = reps[NAMES[0]]

@@ -32,7 +32,7 @@ def child(path, N):
         torch.cuda.synchronize()
         out = {"variant": os.environ.get("SWEEP_VARIANT", "base"),
                "matmat16_ms": e0.elapsed_time(e1) / 10,
-               "hbm_floor_ms": 8 * op.mem_scalars / 6.545e9 * 1e-3 * 1e3 / 1e3}
+               "hbm_floor_ms": 8 * op.mem_scalars / 6.545e12 * 1e3}
         ph = rep.profile_phases_batched(16, iters=10)
         out["phases_ms"] = {r["phase"]: round(r["ms"], 4) for r in ph}
         out["phases_GBps"] = {r["phase"]: round(r["bytes"] / (r["ms"] * 1e-3) / 1e9, 0)
